@@ -245,16 +245,7 @@ class _Handle:
             pass
 
 
-def graph_view(g: dict) -> A.GraphView:
-    gv = A.GraphView()
-    gv.degree = g["degree"]
-    gv.semantic = A.ptr(g["semantic"], A.u32p)
-    gv.keyword = g["keyword"].list_view()
-    gv.logical_ptr = A.ptr(g.get("logical_ptr"), A.u64p)
-    gv.logical = A.ptr(g.get("logical"), A.u32p)
-    gv.norm_order = A.ptr(g.get("norm_order"), A.u32p)
-    gv._keep = g
-    return gv
+graph_view = A.graph_view
 
 
 class RefLib(_Base):

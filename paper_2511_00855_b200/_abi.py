@@ -354,6 +354,19 @@ class Results:
         return self.doc_id[i, :int(self.hit_count[i])]
 
 
+def graph_view(g: dict) -> GraphView:
+    """fg_graph_view over a dict(degree, semantic, keyword: CSR, logical_ptr,
+    logical (E x 4), norm_order); the dict must outlive the view."""
+    gv = GraphView()
+    gv.degree = g["degree"]
+    gv.semantic = ptr(g["semantic"], u32p)
+    gv.keyword = g["keyword"].list_view()
+    gv.logical_ptr = ptr(g.get("logical_ptr"), u64p)
+    gv.logical = ptr(g.get("logical"), u32p)
+    gv.norm_order = ptr(g.get("norm_order"), u32p)
+    return gv
+
+
 def knn_struct(ids, scores, fresh):
     n, k = ids.shape
     return KnnLists(n, k, ptr(ids, u32p), ptr(scores, f64p), ptr(fresh, u8p))

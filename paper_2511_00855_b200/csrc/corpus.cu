@@ -1,0 +1,417 @@
+// corpus.cu — the device DocumentStore, squared norms, query staging and the
+// K1 entry points (batch_scores, pair scores, build_query_vector).
+#include <algorithm>
+#include <cmath>
+#include <thread>
+
+#include "fg_cuda.hpp"
+#include "query_stage.cuh"
+
+namespace fgb {
+namespace {
+
+// finalize_fused (types.cpp:74-79): dense self-dot, then learned, then
+// statistical self sparse dot (every term shared, ascending order).
+__global__ void sqnorm_kernel(DevCorpus c, double* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= c.n) return;
+    const float* row = c.dense + i * c.dstride;
+    double acc = 0.0;
+    for (uint32_t j = 0; j < c.dim; ++j) acc = __fma_rn((double)row[j], (double)row[j], acc);
+    double l = 0.0;
+    for (uint32_t j = 0; j < c.l_nnz[i]; ++j) {
+        const double v = c.l_val[c.l_off[i] + j];
+        l = __fma_rn(v, v, l);
+    }
+    acc = __dadd_rn(acc, l);
+    double s = 0.0;
+    for (uint32_t j = 0; j < c.s_nnz[i]; ++j) {
+        const double v = c.s_val[c.s_off[i] + j];
+        s = __fma_rn(v, v, s);
+    }
+    out[i] = __dadd_rn(acc, s);
+}
+
+// hybrid_score(doc a, doc b) with both rows in global memory: dense chain +
+// merge-join in ascending index order (scoring.cpp:24-42).
+__device__ double sparse_merge(const uint32_t* idx, const float* val, uint64_t oa, uint32_t na,
+                               uint64_t ob, uint32_t nb) {
+    double acc = 0.0;
+    uint32_t i = 0, j = 0;
+    while (i < na && j < nb) {
+        const uint32_t a = idx[oa + i], b = idx[ob + j];
+        if (a < b) {
+            ++i;
+        } else if (b < a) {
+            ++j;
+        } else {
+            acc = __fma_rn((double)val[oa + i], (double)val[ob + j], acc);
+            ++i;
+            ++j;
+        }
+    }
+    return acc;
+}
+
+__global__ void pair_kernel(DevCorpus c, const uint32_t* a, const uint32_t* b, uint64_t m,
+                            double* out) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const uint64_t u = a[t], v = b[t];
+    const float* ru = c.dense + u * c.dstride;
+    const float* rv = c.dense + v * c.dstride;
+    double acc = 0.0;
+    for (uint32_t j = 0; j < c.dim; ++j) acc = __fma_rn((double)ru[j], (double)rv[j], acc);
+    acc = __dadd_rn(acc, sparse_merge(c.l_idx, c.l_val, c.l_off[u], c.l_nnz[u], c.l_off[v], c.l_nnz[v]));
+    acc = __dadd_rn(acc, sparse_merge(c.s_idx, c.s_val, c.s_off[u], c.s_nnz[u], c.s_off[v], c.s_nnz[v]));
+    out[t] = acc;
+}
+
+// batch_scores (scoring.cpp:101-109): every block stages the weighted query
+// in shared memory; one thread per id.
+__global__ void batch_scores_kernel(DevCorpus c, DevQueries q, uint64_t qi, const uint32_t* ids,
+                                    uint64_t m, double* out, uint32_t lcap, uint32_t scap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SmemQuery sq;
+    stage_query(q, qi, c.dstride, smem, lcap, scap, threadIdx.x, blockDim.x, sq,
+                [] { __syncthreads(); });
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t < m) out[t] = hybrid_score(c, sq, ids[t]);
+}
+
+void build_sparse(const fg_sparse_view& sv, uint64_t n, std::vector<uint64_t>& off,
+                  std::vector<uint32_t>& nnz, std::vector<uint32_t>& idx, std::vector<float>& val,
+                  uint32_t& max_nnz, const char* path) {
+    off.resize(n);
+    nnz.resize(n);
+    uint64_t total = 0;
+    max_nnz = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t len = sv.ptr ? sv.ptr[i + 1] - sv.ptr[i] : 0;
+        if (len > 0xFFFFFFFFull) throw Error("invalid-argument", "sparse row too long");
+        off[i] = total;
+        nnz[i] = static_cast<uint32_t>(len);
+        max_nnz = std::max<uint32_t>(max_nnz, nnz[i]);
+        total += round4(nnz[i]);
+    }
+    idx.assign(total, kPad);
+    val.assign(total, 0.0f);
+    for (uint64_t i = 0; i < n; ++i) {
+        if (!nnz[i]) continue;
+        const uint64_t b = sv.ptr[i];
+        for (uint32_t j = 0; j < nnz[i]; ++j) {
+            const uint32_t x = sv.idx[b + j];
+            if (j > 0 && x <= sv.idx[b + j - 1])
+                throw Error("unsorted-sparse", "doc " + std::to_string(i) + ": " + path +
+                                                   " indices must be strictly ascending");
+            idx[off[i] + j] = x;
+            val[off[i] + j] = sv.val[b + j];
+        }
+    }
+}
+
+void copy_list(const fg_list_view& lv, uint64_t n, HostList& out) {
+    out.ptr.assign(n + 1, 0);
+    out.idx.clear();
+    if (!lv.ptr) return;
+    for (uint64_t i = 0; i < n; ++i) out.ptr[i + 1] = lv.ptr[i + 1] - lv.ptr[0];
+    out.idx.assign(lv.idx + lv.ptr[0], lv.idx + lv.ptr[n]);
+}
+
+}  // namespace
+
+void QueryUpload::upload(const fg_query_view& q, cudaStream_t s) {
+    const uint64_t nq = q.count;
+    auto csr = [&](const uint64_t* ptr, const uint32_t* idx, const float* val, DevBuf<uint64_t>& dp,
+                   DevBuf<uint32_t>& di, DevBuf<float>* dv, uint32_t& mx) {
+        std::vector<uint64_t> p(nq + 1, 0);
+        mx = 0;
+        if (ptr)
+            for (uint64_t i = 0; i < nq; ++i) {
+                p[i + 1] = ptr[i + 1] - ptr[0];
+                mx = std::max<uint32_t>(mx, static_cast<uint32_t>(ptr[i + 1] - ptr[i]));
+            }
+        dp.upload(p, s);
+        const uint64_t total = p[nq];
+        di.ensure(std::max<uint64_t>(total, 1));
+        if (total) di.upload(idx + ptr[0], total, s);
+        if (dv) {
+            dv->ensure(std::max<uint64_t>(total, 1));
+            if (total) dv->upload(val + ptr[0], total, s);
+        }
+        h2d_bytes += p.size() * 8 + total * (dv ? 8 : 4);
+    };
+    h2d_bytes = 0;
+    dense.ensure(std::max<uint64_t>(nq * q.dense_dim, 1));
+    dense.upload(q.dense, nq * q.dense_dim, s);
+    std::vector<float4> w(nq);
+    for (uint64_t i = 0; i < nq; ++i)
+        w[i] = q.weights ? make_float4(q.weights[i].dense, q.weights[i].learned,
+                                       q.weights[i].statistical, q.weights[i].entity)
+                         : make_float4(1.f, 1.f, 1.f, 0.f);
+    weights.upload(w, s);
+    csr(q.learned.ptr, q.learned.idx, q.learned.val, l_ptr, l_idx, &l_val, max_lnnz);
+    csr(q.statistical.ptr, q.statistical.idx, q.statistical.val, s_ptr, s_idx, &s_val, max_snnz);
+    csr(q.required_keywords.ptr, q.required_keywords.idx, nullptr, req_ptr, req_idx, nullptr, max_req);
+    auto per = [&](const uint32_t* src, uint32_t dflt, DevBuf<uint32_t>& dst, uint32_t& mx) {
+        std::vector<uint32_t> v(nq);
+        mx = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            v[i] = src ? src[i] : dflt;
+            mx = std::max(mx, v[i]);
+        }
+        dst.upload(v, s);
+        h2d_bytes += nq * 4;
+    };
+    uint32_t mh = 0;
+    per(q.k, 10, k, max_k);
+    per(q.beam_width, 64, beam, max_beam);
+    per(q.max_entity_hops, 2, hops, mh);
+    h2d_bytes += nq * q.dense_dim * 4 + nq * 16;
+    dq = DevQueries{nq,         q.dense_dim, dense.get(),   weights.get(), l_ptr.get(),
+                    l_idx.get(), l_val.get(), s_ptr.get(),   s_idx.get(),   s_val.get(),
+                    req_ptr.get(), req_idx.get(), k.get(),    beam.get(),    hops.get()};
+}
+
+// Bytes of shared memory stage_query needs for hash capacities lcap/scap.
+size_t stage_bytes(uint32_t dstride, uint32_t lcap, uint32_t scap) {
+    return static_cast<size_t>(dstride) * 4 + static_cast<size_t>(lcap + scap) * 8;
+}
+
+}  // namespace fgb
+
+using namespace fgb;
+
+extern "C" {
+
+int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
+    return guarded([&] {
+        if (!v || !out) throw Error("invalid-argument", "null pointer");
+        if (v->n == 0) throw Error("empty-corpus", "corpus holds no documents");
+        if (v->n >= 0x7FFFFFFFull) throw Error("invalid-argument", "corpus exceeds 2^31-1 nodes");
+        require_device(device);
+        auto c = std::make_unique<fg_corpus>();
+        c->device = device;
+        c->n = v->n;
+        c->dim = v->dense_dim;
+        c->dstride = round4(std::max<uint32_t>(v->dense_dim, 1));
+        FGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        cudaStream_t s = c->stream;
+        const uint64_t n = v->n;
+
+        // dense rows, zero padded to 16 B
+        if (c->dstride == c->dim) {
+            c->dense.upload(v->dense, n * c->dim, s);
+        } else {
+            std::vector<float> pad(n * c->dstride, 0.0f);
+            for (uint64_t i = 0; i < n; ++i)
+                std::memcpy(pad.data() + i * c->dstride, v->dense + i * c->dim, c->dim * 4);
+            c->dense.upload(pad, s);
+        }
+        {
+            std::vector<uint64_t> off;
+            std::vector<uint32_t> nnz, idx;
+            std::vector<float> val;
+            build_sparse(v->learned, n, off, nnz, idx, val, c->max_lnnz, "learned");
+            c->l_off.upload(off, s);
+            c->l_nnz.upload(nnz, s);
+            c->l_idx.upload(idx.empty() ? std::vector<uint32_t>(4, kPad) : idx, s);
+            c->l_val.upload(val.empty() ? std::vector<float>(4, 0.f) : val, s);
+            FGB_CUDA(cudaStreamSynchronize(s));
+            build_sparse(v->statistical, n, off, nnz, idx, val, c->max_snnz, "statistical");
+            c->s_off.upload(off, s);
+            c->s_nnz.upload(nnz, s);
+            c->s_idx.upload(idx.empty() ? std::vector<uint32_t>(4, kPad) : idx, s);
+            c->s_val.upload(val.empty() ? std::vector<float>(4, 0.f) : val, s);
+            FGB_CUDA(cudaStreamSynchronize(s));
+        }
+        // keywords default to the statistical support (corpus.cpp:116)
+        if (v->keywords.ptr) {
+            copy_list(v->keywords, n, c->keywords);
+        } else {
+            fg_list_view kv{v->statistical.ptr, v->statistical.idx};
+            copy_list(kv, n, c->keywords);
+        }
+        copy_list(v->entities, n, c->entities);
+        for (uint64_t i = 0; i < n; ++i) {
+            if (!std::is_sorted(c->entities.begin(i), c->entities.end(i)) ||
+                !std::is_sorted(c->keywords.begin(i), c->keywords.end(i)))
+                throw Error("unsorted-sparse", "doc " + std::to_string(i) +
+                                                   ": keyword/entity lists must be sorted");
+        }
+        c->kw_ptr.upload(c->keywords.ptr, s);
+        c->kw_idx.upload(c->keywords.idx.empty() ? std::vector<uint32_t>(1, 0) : c->keywords.idx, s);
+        c->ent_ptr.upload(c->entities.ptr, s);
+        c->ent_idx.upload(c->entities.idx.empty() ? std::vector<uint32_t>(1, 0) : c->entities.idx, s);
+        c->doc_id.resize(n);
+        for (uint64_t i = 0; i < n; ++i) c->doc_id[i] = v->doc_id ? v->doc_id[i] : i;
+        c->deleted_h.assign(n, 0);
+        if (v->deleted)
+            for (uint64_t i = 0; i < n; ++i) c->deleted_h[i] = v->deleted[i] ? 1 : 0;
+        c->deleted.upload(c->deleted_h, s);
+        c->sqnorm.alloc(n);
+
+        c->dc = DevCorpus{n,
+                          c->dim,
+                          c->dstride,
+                          c->dense.get(),
+                          c->l_off.get(),
+                          c->l_nnz.get(),
+                          c->l_idx.get(),
+                          c->l_val.get(),
+                          c->s_off.get(),
+                          c->s_nnz.get(),
+                          c->s_idx.get(),
+                          c->s_val.get(),
+                          c->kw_ptr.get(),
+                          c->kw_idx.get(),
+                          c->ent_ptr.get(),
+                          c->ent_idx.get(),
+                          c->sqnorm.get(),
+                          c->deleted.get()};
+        sqnorm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->sqnorm.get());
+        FGB_LAUNCH("sqnorm_kernel");
+        c->sqnorm_h.resize(n);
+        c->sqnorm.download(c->sqnorm_h.data(), n, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        *out = c.release();
+    });
+}
+
+int fg_corpus_free(fg_corpus* c) {
+    if (c) {
+        cudaSetDevice(c->device);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        delete c;
+    }
+    return FG_OK;
+}
+
+int fg_corpus_size(const fg_corpus* c, uint64_t* n, uint32_t* dim) {
+    return guarded([&] {
+        if (!c) throw Error("invalid-argument", "null corpus");
+        if (n) *n = c->n;
+        if (dim) *dim = c->dim;
+    });
+}
+
+int fg_corpus_sqnorm(const fg_corpus* c, double* out) {
+    return guarded([&] { std::copy(c->sqnorm_h.begin(), c->sqnorm_h.end(), out); });
+}
+
+int fg_corpus_set_deleted(fg_corpus* c, const uint8_t* flags) {
+    return guarded([&] {
+        FGB_CUDA(cudaSetDevice(c->device));
+        for (uint64_t i = 0; i < c->n; ++i) c->deleted_h[i] = flags[i] ? 1 : 0;
+        c->deleted.upload(c->deleted_h, c->stream);
+        FGB_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// build_query_vector (corpus.cpp:86-103) on the host: the fp32 products the
+// kernels apply in-register, exposed for the fusion-weight API and tests.
+int fg_build_query_vector(const fg_query_view* q, uint64_t i, float* dense_out, uint32_t* lnnz,
+                          float* lval, uint32_t* snnz, float* sval, double* sqnorm) {
+    return guarded([&] {
+        if (!q || i >= q->count) throw Error("invalid-argument", "query index out of range");
+        const fg_weights w = q->weights ? q->weights[i] : fg_weights{1.f, 1.f, 1.f, 0.f};
+        const float* x = q->dense + i * q->dense_dim;
+        double acc = 0.0;
+        for (uint32_t j = 0; j < q->dense_dim; ++j) {
+            dense_out[j] = w.dense * x[j];
+            acc += static_cast<double>(dense_out[j]) * static_cast<double>(dense_out[j]);
+        }
+        auto scale = [&](const fg_sparse_view& sv, float wt, uint32_t* nnz, float* out) {
+            double a = 0.0;
+            *nnz = 0;
+            if (!sv.ptr || wt == 0.0f) return a;
+            const uint64_t b = sv.ptr[i], e = sv.ptr[i + 1];
+            for (uint64_t j = b; j < e; ++j) {
+                out[j - b] = wt * sv.val[j];
+                a += static_cast<double>(out[j - b]) * static_cast<double>(out[j - b]);
+            }
+            *nnz = static_cast<uint32_t>(e - b);
+            return a;
+        };
+        const double l = scale(q->learned, w.learned, lnnz, lval);
+        const double s = scale(q->statistical, w.statistical, snnz, sval);
+        acc += l;
+        acc += s;
+        if (sqnorm) *sqnorm = acc;
+    });
+}
+
+int fg_batch_scores(const fg_corpus* c, const fg_query_view* q, uint64_t qi, const uint32_t* ids,
+                    uint64_t m, double* out) {
+    return guarded([&] {
+        if (!c || !q || qi >= q->count) throw Error("invalid-argument", "bad query");
+        FGB_CUDA(cudaSetDevice(c->device));
+        if (q->dense_dim != c->dim)
+            throw Error("dim-mismatch", "dense dimensions differ: " + std::to_string(q->dense_dim) +
+                                            " vs " + std::to_string(c->dim));
+        for (uint64_t i = 0; i < m; ++i)
+            if (ids[i] >= c->n)
+                throw Error("unknown-id", "node " + std::to_string(ids[i]) + " out of range");
+        if (m == 0) return;
+        cudaStream_t s = c->stream;
+        // single-query sub-view
+        fg_query_view one = *q;
+        one.count = 1;
+        one.dense = q->dense + qi * q->dense_dim;
+        uint64_t lp[2], sp[2];
+        if (q->learned.ptr) {
+            lp[0] = q->learned.ptr[qi];
+            lp[1] = q->learned.ptr[qi + 1];
+            one.learned.ptr = lp;
+        }
+        if (q->statistical.ptr) {
+            sp[0] = q->statistical.ptr[qi];
+            sp[1] = q->statistical.ptr[qi + 1];
+            one.statistical.ptr = sp;
+        }
+        if (q->weights) one.weights = q->weights + qi;
+        one.required_keywords = {nullptr, nullptr};
+        one.entities = {nullptr, nullptr};
+        one.k = nullptr;
+        one.beam_width = nullptr;
+        one.max_entity_hops = nullptr;
+        QueryUpload up;
+        up.upload(one, s);
+        DevBuf<uint32_t> d_ids;
+        d_ids.upload(ids, m, s);
+        DevBuf<double> d_out(m);
+        const uint32_t lcap = hash_capacity(up.max_lnnz), scap = hash_capacity(up.max_snnz);
+        const size_t sm = stage_bytes(c->dstride, lcap, scap);
+        if (sm > 48 * 1024)
+            FGB_CUDA(cudaFuncSetAttribute(batch_scores_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        batch_scores_kernel<<<(unsigned)((m + 127) / 128), 128, sm, s>>>(c->dc, up.dq, 0, d_ids.get(), m,
+                                                                     d_out.get(), lcap, scap);
+        FGB_LAUNCH("batch_scores_kernel");
+        d_out.download(out, m, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int fg_pair_scores(const fg_corpus* c, const uint32_t* a, const uint32_t* b, uint64_t m,
+                   double* out) {
+    return guarded([&] {
+        if (!c) throw Error("invalid-argument", "null corpus");
+        FGB_CUDA(cudaSetDevice(c->device));
+        for (uint64_t i = 0; i < m; ++i)
+            if (a[i] >= c->n || b[i] >= c->n)
+                throw Error("unknown-id", "node out of range");
+        if (m == 0) return;
+        cudaStream_t s = c->stream;
+        DevBuf<uint32_t> da, db;
+        da.upload(a, m, s);
+        db.upload(b, m, s);
+        DevBuf<double> d_out(m);
+        pair_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(c->dc, da.get(), db.get(), m, d_out.get());
+        FGB_LAUNCH("pair_kernel");
+        d_out.download(out, m, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+}  // extern "C"

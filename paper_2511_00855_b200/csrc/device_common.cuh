@@ -1,0 +1,225 @@
+// device_common.cuh — device-side layout of the corpus and the bit-exact
+// hybrid distance (K1), shared by every kernel.
+//
+// Parity contract (scoring.cpp:10-99): a hybrid score is
+//     acc  = sum_i (double)q_i * (double)d_i        (index order)
+//     acc += sum_{shared t, ascending} (double)ql_t * (double)dl_t
+//     acc += sum_{shared t, ascending} (double)qs_t * (double)ds_t
+// with every product exact in fp64 (fp32 x fp32 fits in 48 bits) and every
+// sum rounded once.  We evaluate each sum as a sequential chain of
+// __fma_rn(a, b, acc) — exact product + one rounding, identical to the
+// reference's `acc += a * b` — in the same order, so every score is
+// BIT-IDENTICAL to fusegraph::hybrid_score.  One thread owns one
+// (query, candidate) chain; parallelism comes from many candidates.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace fgb {
+
+constexpr uint32_t kPad = 0xFFFFFFFFu;    // padding index in sparse rows
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash slot
+
+// DocumentStore on HBM (types.hpp:119-133), structure-of-arrays:
+//  dense   n x dstride fp32, dstride = dim rounded up to 4 (16-B rows, zero pad)
+//  sparse  per path: row offset (multiple of 4 entries) + nnz, idx/val arrays
+//          padded per row to a multiple of 4 with (kPad, 0) so rows load as
+//          uint4/float4
+//  keywords, entities: plain CSR (sorted ids per doc)
+struct DevCorpus {
+    uint64_t n;
+    uint32_t dim, dstride;
+    const float* dense;
+    const uint64_t* l_off;
+    const uint32_t* l_nnz;
+    const uint32_t* l_idx;
+    const float* l_val;
+    const uint64_t* s_off;
+    const uint32_t* s_nnz;
+    const uint32_t* s_idx;
+    const float* s_val;
+    const uint64_t* kw_ptr;
+    const uint32_t* kw_idx;
+    const uint64_t* ent_ptr;
+    const uint32_t* ent_idx;
+    const double* sqnorm;
+    const uint8_t* deleted;
+};
+
+// ---------------------------------------------------------------- hashing
+__device__ __forceinline__ uint32_t hslot(uint32_t key, uint32_t mask) {
+    return (key * 2654435761u) & mask;  // mask = capacity - 1 (power of two)
+}
+
+// Insert key->val into an open-addressing table (keys pre-set to kEmpty).
+// Keys are unique per table (strictly ascending sparse indices).
+__device__ __forceinline__ void hash_insert(uint32_t* keys, float* vals, uint32_t mask,
+                                            uint32_t key, float val) {
+    uint32_t s = hslot(key, mask);
+    while (true) {
+        const uint32_t prev = atomicCAS(&keys[s], kEmpty, key);
+        if (prev == kEmpty || prev == key) {
+            vals[s] = val;
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+__device__ __forceinline__ bool hash_find(const uint32_t* keys, const float* vals, uint32_t mask,
+                                          uint32_t key, float& out) {
+    uint32_t s = hslot(key, mask);
+    while (true) {
+        const uint32_t k = keys[s];
+        if (k == key) {
+            out = vals[s];
+            return true;
+        }
+        if (k == kEmpty) return false;
+        s = (s + 1) & mask;
+    }
+}
+
+__host__ __device__ inline uint32_t hash_capacity(uint32_t nnz) {
+    uint32_t c = 16;
+    while (c < 2 * nnz) c <<= 1;
+    return c;
+}
+
+// A weighted query (or a document acting as one) staged in shared memory:
+// dense part (dstride floats, zero padded) and one hash per sparse path.
+struct SmemQuery {
+    const float* dense;  // nullptr: dense path disabled (weight 0) -> contributes +0.0
+    const uint32_t* lkeys;
+    const float* lvals;
+    uint32_t lmask;      // 0: learned path empty/disabled
+    const uint32_t* skeys;
+    const float* svals;
+    uint32_t smask;
+};
+
+// Dense dot of the staged query against row `node`, sequential over i.
+__device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q, uint64_t node) {
+    const float4* row = reinterpret_cast<const float4*>(c.dense + node * c.dstride);
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    const uint32_t n4 = c.dstride >> 2;
+    double acc = 0.0;
+    uint32_t i = 0;
+    for (; i + 4 <= n4; i += 4) {
+        float4 d[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = __ldg(row + i + j);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float4 qq = q4[i + j];
+            acc = __fma_rn((double)qq.x, (double)d[j].x, acc);
+            acc = __fma_rn((double)qq.y, (double)d[j].y, acc);
+            acc = __fma_rn((double)qq.z, (double)d[j].z, acc);
+            acc = __fma_rn((double)qq.w, (double)d[j].w, acc);
+        }
+    }
+    for (; i < n4; ++i) {
+        const float4 d = __ldg(row + i);
+        const float4 qq = q4[i];
+        acc = __fma_rn((double)qq.x, (double)d.x, acc);
+        acc = __fma_rn((double)qq.y, (double)d.y, acc);
+        acc = __fma_rn((double)qq.z, (double)d.z, acc);
+        acc = __fma_rn((double)qq.w, (double)d.w, acc);
+    }
+    return acc;
+}
+
+// Sparse dot: walk the document row in ascending index order and probe the
+// query's hash; matches accumulate in ascending shared-index order, exactly
+// the merge/probe order of sparse_dot_impl (scoring.cpp:24-74).
+__device__ __forceinline__ double sparse_chain(const uint32_t* idx, const float* val, uint64_t off,
+                                               uint32_t nnz, const uint32_t* keys,
+                                               const float* vals, uint32_t mask) {
+    double acc = 0.0;
+    const uint4* i4 = reinterpret_cast<const uint4*>(idx + off);
+    const float4* v4 = reinterpret_cast<const float4*>(val + off);
+    const uint32_t n4 = (nnz + 3) >> 2;
+    for (uint32_t i = 0; i < n4; ++i) {
+        const uint4 ii = __ldg(i4 + i);
+        const float4 vv = __ldg(v4 + i);
+        float q;
+        if (ii.x != kPad && hash_find(keys, vals, mask, ii.x, q)) acc = __fma_rn((double)q, (double)vv.x, acc);
+        if (ii.y != kPad && hash_find(keys, vals, mask, ii.y, q)) acc = __fma_rn((double)q, (double)vv.y, acc);
+        if (ii.z != kPad && hash_find(keys, vals, mask, ii.z, q)) acc = __fma_rn((double)q, (double)vv.z, acc);
+        if (ii.w != kPad && hash_find(keys, vals, mask, ii.w, q)) acc = __fma_rn((double)q, (double)vv.w, acc);
+    }
+    return acc;
+}
+
+// hybrid_score(weighted query, doc) (scoring.cpp:88-99): dense, then learned,
+// then statistical, in that fixed order.
+__device__ __forceinline__ double hybrid_score(const DevCorpus& c, const SmemQuery& q,
+                                               uint64_t node) {
+    double acc = q.dense ? dense_chain(c, q.dense, node) : 0.0;
+    if (q.lmask) {
+        const double l = sparse_chain(c.l_idx, c.l_val, c.l_off[node], c.l_nnz[node], q.lkeys,
+                                      q.lvals, q.lmask);
+        acc = __dadd_rn(acc, l);
+    } else {
+        acc = __dadd_rn(acc, 0.0);
+    }
+    if (q.smask) {
+        const double s = sparse_chain(c.s_idx, c.s_val, c.s_off[node], c.s_nnz[node], q.skeys,
+                                      q.svals, q.smask);
+        acc = __dadd_rn(acc, s);
+    } else {
+        acc = __dadd_rn(acc, 0.0);
+    }
+    return acc;
+}
+
+// Sorted-list membership (sorted_contains, types.cpp:86-88).
+__device__ __forceinline__ bool sorted_contains(const uint32_t* a, uint64_t b, uint64_t e,
+                                               uint32_t x) {
+    while (b < e) {
+        const uint64_t m = (b + e) >> 1;
+        const uint32_t v = a[m];
+        if (v < x)
+            b = m + 1;
+        else if (v > x)
+            e = m;
+        else
+            return true;
+    }
+    return false;
+}
+
+// SplitMix64 / mix_seed / bounded (rng.hpp:17-41) on the device.
+struct DevRng {
+    uint64_t state;
+    __device__ explicit DevRng(uint64_t seed) : state(seed) {}
+    __device__ uint64_t next() {
+        uint64_t z = (state += 0x9E3779B97F4A7C15ULL);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+};
+__device__ __forceinline__ uint64_t dev_mix_seed(uint64_t seed, uint64_t stream) {
+    DevRng m(seed ^ (0xA0761D6478BD642FULL * (stream + 1)));
+    return m.next();
+}
+__device__ __forceinline__ uint64_t dev_bounded(DevRng& r, uint64_t bound) {
+    return __umul64hi(r.next(), bound);
+}
+
+// KnnEntry ordering `better` (knn_graph.cpp:15-18): score desc, id asc.
+__device__ __forceinline__ bool better(double sa, uint32_t ia, double sb, uint32_t ib) {
+    return sa != sb ? sa > sb : ia < ib;
+}
+
+// Orderable key of a double: ascending u64 order == ascending double order
+// (no NaNs on this path).
+__device__ __forceinline__ uint64_t order_key(double d) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(d));
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+}  // namespace fgb

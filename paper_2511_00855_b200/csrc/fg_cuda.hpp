@@ -1,0 +1,164 @@
+// fg_cuda.hpp — host-side CUDA plumbing: checked calls, owning device
+// buffers, the fg_corpus handle, and the device query batch.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+#include "fg_internal.hpp"
+
+namespace fgb {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (e == cudaErrorMemoryAllocation)
+            throw Error("out-of-memory", std::string(what) + ": " + cudaGetErrorString(e));
+        throw Error("cuda-error", std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define FGB_CUDA(x) ::fgb::cuda_check((x), #x)
+#define FGB_LAUNCH(what) ::fgb::cuda_check(cudaGetLastError(), what)
+
+inline void require_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw Error("no-cuda-device", "no CUDA device is visible (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= n)
+        throw Error("no-cuda-device", "device " + std::to_string(device) + " out of range");
+    FGB_CUDA(cudaSetDevice(device));
+}
+
+// Owning device allocation.
+template <typename T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(size_t n) { alloc(n); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+
+    void alloc(size_t n) {
+        release();
+        n_ = n;
+        if (n) FGB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    }
+    void ensure(size_t n) {
+        if (n > n_) alloc(n);
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    void upload(const T* src, size_t n, cudaStream_t s = 0) {
+        ensure(n);
+        if (n) FGB_CUDA(cudaMemcpyAsync(p_, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+    void upload(const std::vector<T>& v, cudaStream_t s = 0) { upload(v.data(), v.size(), s); }
+    void download(T* dst, size_t n, cudaStream_t s = 0) const {
+        if (n) FGB_CUDA(cudaMemcpyAsync(dst, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    }
+    void zero(cudaStream_t s = 0) {
+        if (n_) FGB_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s));
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// Host-side CSR copy of a sorted-id list per row.
+struct HostList {
+    std::vector<uint64_t> ptr{0};
+    std::vector<uint32_t> idx;
+    size_t rows() const { return ptr.size() - 1; }
+    const uint32_t* begin(size_t r) const { return idx.data() + ptr[r]; }
+    const uint32_t* end(size_t r) const { return idx.data() + ptr[r + 1]; }
+    size_t len(size_t r) const { return ptr[r + 1] - ptr[r]; }
+};
+
+}  // namespace fgb
+
+// The device mirror of a DocumentStore.
+struct fg_corpus {
+    int device = 0;
+    uint64_t n = 0;
+    uint32_t dim = 0, dstride = 0;
+    uint32_t max_lnnz = 0, max_snnz = 0;
+    fgb::DevCorpus dc{};
+    fgb::DevBuf<float> dense, l_val, s_val;
+    fgb::DevBuf<uint64_t> l_off, s_off, kw_ptr, ent_ptr;
+    fgb::DevBuf<uint32_t> l_nnz, s_nnz, l_idx, s_idx, kw_idx, ent_idx;
+    fgb::DevBuf<double> sqnorm;
+    fgb::DevBuf<uint8_t> deleted;
+    // host copies used by host-side stages (entity map, logical edges, seeds)
+    std::vector<uint64_t> doc_id;
+    std::vector<uint8_t> deleted_h;
+    fgb::HostList keywords, entities;
+    std::vector<double> sqnorm_h;
+    cudaStream_t stream = nullptr;
+};
+
+namespace fgb {
+
+// A query batch on the device (raw vectors; weights applied in-kernel with
+// the reference's fp32 product, corpus.cpp:89,96).
+struct DevQueries {
+    uint64_t count;
+    uint32_t dim;
+    const float* dense;     // count * dim
+    const float4* weights;  // (dense, learned, statistical, entity)
+    const uint64_t* l_ptr;
+    const uint32_t* l_idx;
+    const float* l_val;
+    const uint64_t* s_ptr;
+    const uint32_t* s_idx;
+    const float* s_val;
+    const uint64_t* req_ptr;
+    const uint32_t* req_idx;
+    const uint32_t* k;
+    const uint32_t* beam;
+    const uint32_t* hops;
+};
+
+// Owning device copy of an fg_query_view (missing CSRs become empty rows).
+struct QueryUpload {
+    DevBuf<float> dense, l_val, s_val;
+    DevBuf<float4> weights;
+    DevBuf<uint64_t> l_ptr, s_ptr, req_ptr;
+    DevBuf<uint32_t> l_idx, s_idx, req_idx, k, beam, hops;
+    uint32_t max_lnnz = 0, max_snnz = 0, max_req = 0, max_k = 0, max_beam = 0;
+    uint64_t h2d_bytes = 0;
+    DevQueries dq{};
+
+    void upload(const fg_query_view& q, cudaStream_t s);
+};
+
+inline uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+}  // namespace fgb

@@ -1,0 +1,477 @@
+// knn.cu — K3: NN-Descent on the GPU (knn_graph.cpp:52-166).
+//
+// One pass is three device stages, double-buffered like the reference:
+//   1. reverse lists: every forward entry (u -> v, score, fresh) is sorted by
+//      (target v, score desc, source u asc) with two stable CUB radix sorts,
+//      and each target keeps its first k (knn_graph.cpp:78-89);
+//   2. one CTA per node u gathers the two-hop pool through forward+reverse
+//      lists into a shared-memory hash set (OR-ing path freshness,
+//      knn_graph.cpp:94-120), drops u's own list members, and scores every
+//      surviving candidate bit-exactly, one thread per candidate, against u
+//      staged in shared memory (pair_score, knn_graph.cpp:20-22);
+//   3. candidates that beat the running k-th entry merge into a sorted top-k
+//      kept in shared memory (better: score desc, id asc); the result and the
+//      replaced count are written to the next buffer (knn_graph.cpp:122-141).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "fg_cuda.hpp"
+#include "knn.cuh"
+#include "stage_doc.cuh"
+
+namespace fgb {
+namespace {
+
+constexpr int kPassThreads = 512;
+
+// Rejection sampling (knn_graph.cpp:28-36) when 4k < n.
+__global__ void knn_sample_kernel(uint64_t n, uint32_t k, uint64_t seed, uint32_t* ids) {
+    const uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    DevRng rng(dev_mix_seed(seed, u));
+    uint32_t* picks = ids + u * k;
+    uint32_t cnt = 0;
+    while (cnt < k) {
+        const uint32_t cand = static_cast<uint32_t>(dev_bounded(rng, n));
+        if (cand == u) continue;
+        bool dup = false;
+        for (uint32_t j = 0; j < cnt; ++j) dup |= picks[j] == cand;
+        if (dup) continue;
+        picks[cnt++] = cand;
+    }
+}
+
+// Scores the k picks of u and sorts them by `better` (knn_graph.cpp:63-72).
+__global__ void knn_init_score_kernel(DevCorpus c, uint32_t k, uint32_t* ids, double* scores,
+                                      uint8_t* fresh, uint32_t lcap, uint32_t scap) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint64_t u = blockIdx.x;
+    SmemQuery sq;
+    stage_doc(c, u, smem, lcap, scap, threadIdx.x, blockDim.x, sq, [] { __syncthreads(); });
+    double* sc = reinterpret_cast<double*>(smem + doc_stage_bytes(c.dstride, lcap, scap));
+    uint32_t* id = reinterpret_cast<uint32_t*>(sc + k);
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+        id[j] = ids[u * k + j];
+        sc[j] = hybrid_score(c, sq, id[j]);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < k; j += blockDim.x) {
+        uint32_t pos = 0;
+        for (uint32_t i = 0; i < k; ++i) pos += better(sc[i], id[i], sc[j], id[j]);
+        ids[u * k + pos] = id[j];
+        scores[u * k + pos] = sc[j];
+        fresh[u * k + pos] = 1;
+    }
+}
+
+__global__ void score_keys_kernel(const double* scores, uint64_t m, uint64_t* keys,
+                                  uint32_t* vals) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    keys[i] = order_key(scores[i]);
+    vals[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void target_keys_kernel(const uint32_t* ids, const uint32_t* order, uint64_t m,
+                                   uint32_t* keys, uint32_t* cnt) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const uint32_t t = ids[order[i]];
+    keys[i] = t;
+    atomicAdd(&cnt[t], 1u);
+}
+
+// R[v] = first min(k, cnt) entries of v's segment (sorted score desc, u asc).
+__global__ void reverse_fill_kernel(uint64_t n, uint32_t k, const uint32_t* order,
+                                    const uint32_t* cnt, const uint32_t* start,
+                                    const uint8_t* fresh, uint32_t* rids, uint8_t* rfresh,
+                                    uint32_t* rcnt) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n * k) return;
+    const uint64_t v = t / k;
+    const uint32_t j = static_cast<uint32_t>(t % k);
+    const uint32_t c = min(cnt[v], k);
+    if (j == 0) rcnt[v] = c;
+    if (j >= c) return;
+    const uint32_t e = order[start[v] + j];
+    rids[t] = e / k;
+    rfresh[t] = fresh[e];
+}
+
+struct PassArgs {
+    DevCorpus c;
+    uint32_t k;
+    const uint32_t* L_ids;
+    const double* L_sc;
+    const uint8_t* L_fr;
+    const uint32_t* R_ids;
+    const uint8_t* R_fr;
+    const uint32_t* R_cnt;
+    uint32_t* N_ids;
+    double* N_sc;
+    uint8_t* N_fr;
+    unsigned long long* changed;
+    uint32_t pool_cap;  // power of two
+    uint32_t lcap, scap;
+};
+
+__device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uint32_t mask,
+                                            uint32_t id, bool fresh) {
+    uint32_t s = hslot(id, mask);
+    while (true) {
+        const uint32_t prev = atomicCAS(&keys[s], kEmpty, id);
+        if (prev == kEmpty || prev == id) break;
+        s = (s + 1) & mask;
+    }
+    if (fresh) atomicOr(&fbits[s >> 5], 1u << (s & 31));
+}
+
+// One NN-Descent pass for node u = blockIdx.x.
+__global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t k = a.k;
+    const uint64_t u = blockIdx.x;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    SmemQuery sq;
+    unsigned char* p = smem + ((doc_stage_bytes(a.c.dstride, a.lcap, a.scap) + 15) & ~size_t(15));
+    uint32_t* keys = reinterpret_cast<uint32_t*>(p);
+    uint32_t* fbits = keys + a.pool_cap;
+    uint32_t* hbits = fbits + a.pool_cap / 32;  // "already in L[u]"
+    double* T_sc = reinterpret_cast<double*>(hbits + a.pool_cap / 32);
+    double* T2_sc = T_sc + k;
+    double* S_sc = T2_sc + k;
+    uint32_t* T_id = reinterpret_cast<uint32_t*>(S_sc + nt);
+    uint32_t* T2_id = T_id + k;
+    uint32_t* S_id = T2_id + k;
+    uint8_t* T_new = reinterpret_cast<uint8_t*>(S_id + nt);
+    uint8_t* T2_new = T_new + k;
+    __shared__ uint32_t S_cnt;
+    const uint32_t mask = a.pool_cap - 1;
+
+    for (uint32_t j = tid; j < a.pool_cap; j += nt) keys[j] = kEmpty;
+    for (uint32_t j = tid; j < a.pool_cap / 32; j += nt) {
+        fbits[j] = 0;
+        hbits[j] = 0;
+    }
+    for (uint32_t j = tid; j < k; j += nt) {
+        T_id[j] = a.L_ids[u * k + j];
+        T_sc[j] = a.L_sc[u * k + j];
+        T_new[j] = 0;
+    }
+    if (tid == 0) S_cnt = 0;
+    stage_doc(a.c, u, smem, a.lcap, a.scap, tid, nt, sq, [] { __syncthreads(); });
+
+    // L[u] members: mark as "have" (their scores are known; knn_graph.cpp:122-131)
+    for (uint32_t j = tid; j < k; j += nt) {
+        const uint32_t id = T_id[j];
+        uint32_t s = hslot(id, mask);
+        while (true) {
+            const uint32_t prev = atomicCAS(&keys[s], kEmpty, id);
+            if (prev == kEmpty || prev == id) break;
+            s = (s + 1) & mask;
+        }
+        atomicOr(&hbits[s >> 5], 1u << (s & 31));
+    }
+    __syncthreads();
+
+    // Two-hop pool through forward + reverse adjacency (knn_graph.cpp:97-110).
+    const uint32_t rc_u = a.R_cnt[u];
+    const uint32_t nh1 = k + rc_u;
+    const uint64_t items = static_cast<uint64_t>(nh1) * (2 * k);
+    for (uint64_t it = tid; it < items; it += nt) {
+        const uint32_t h = static_cast<uint32_t>(it / (2 * k));
+        const uint32_t j = static_cast<uint32_t>(it % (2 * k));
+        uint32_t h1;
+        bool f1;
+        if (h < k) {
+            h1 = a.L_ids[u * k + h];
+            f1 = a.L_fr[u * k + h];
+        } else {
+            h1 = a.R_ids[u * k + (h - k)];
+            f1 = a.R_fr[u * k + (h - k)];
+        }
+        uint32_t h2;
+        bool f2;
+        if (j < k) {
+            h2 = a.L_ids[(uint64_t)h1 * k + j];
+            f2 = a.L_fr[(uint64_t)h1 * k + j];
+        } else {
+            const uint32_t jj = j - k;
+            if (jj >= a.R_cnt[h1]) continue;
+            h2 = a.R_ids[(uint64_t)h1 * k + jj];
+            f2 = a.R_fr[(uint64_t)h1 * k + jj];
+        }
+        if (h2 == u) continue;
+        pool_insert(keys, fbits, mask, h2, f1 || f2);
+    }
+    __syncthreads();
+
+    // Score fresh, new candidates; merge survivors into the running top-k.
+    for (uint32_t base = 0; base < a.pool_cap; base += nt) {
+        const uint32_t s = base + tid;
+        const uint32_t id = s < a.pool_cap ? keys[s] : kEmpty;
+        const bool cand = id != kEmpty && ((fbits[s >> 5] >> (s & 31)) & 1u) &&
+                          !((hbits[s >> 5] >> (s & 31)) & 1u);
+        if (cand) {
+            const double sc = hybrid_score(a.c, sq, id);
+            if (better(sc, id, T_sc[k - 1], T_id[k - 1])) {
+                const uint32_t slot = atomicAdd(&S_cnt, 1u);
+                S_sc[slot] = sc;
+                S_id[slot] = id;
+            }
+        }
+        __syncthreads();
+        const uint32_t m = S_cnt;
+        __syncthreads();  // everyone holds m before S_cnt can change again
+        if (m == 0) continue;
+        // rank-merge T (sorted) with S (unsorted); ids are pairwise distinct
+        for (uint32_t i = tid; i < k; i += nt) {
+            uint32_t pos = i;
+            for (uint32_t q = 0; q < m; ++q) pos += better(S_sc[q], S_id[q], T_sc[i], T_id[i]);
+            if (pos < k) {
+                T2_sc[pos] = T_sc[i];
+                T2_id[pos] = T_id[i];
+                T2_new[pos] = T_new[i];
+            }
+        }
+        for (uint32_t i = tid; i < m; i += nt) {
+            uint32_t pos = 0;
+            for (uint32_t q = 0; q < m; ++q) pos += better(S_sc[q], S_id[q], S_sc[i], S_id[i]);
+            uint32_t lo = 0, hi = k;  // #T entries better than S[i]
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (better(T_sc[mid], T_id[mid], S_sc[i], S_id[i]))
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            pos += lo;
+            if (pos < k) {
+                T2_sc[pos] = S_sc[i];
+                T2_id[pos] = S_id[i];
+                T2_new[pos] = 1;
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < k; i += nt) {
+            T_sc[i] = T2_sc[i];
+            T_id[i] = T2_id[i];
+            T_new[i] = T2_new[i];
+        }
+        if (tid == 0) S_cnt = 0;
+        __syncthreads();
+    }
+
+    uint32_t mine = 0;
+    for (uint32_t i = tid; i < k; i += nt) {
+        a.N_ids[u * k + i] = T_id[i];
+        a.N_sc[u * k + i] = T_sc[i];
+        a.N_fr[u * k + i] = T_new[i];  // old entries participated (fresh=false)
+        mine += T_new[i];
+    }
+    mine = __reduce_add_sync(0xFFFFFFFFu, mine);
+    if ((tid & 31) == 0 && mine) atomicAdd(a.changed, (unsigned long long)mine);
+}
+
+size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap) {
+    size_t b = (doc_stage_bytes(dstride, lcap, scap) + 15) & ~size_t(15);
+    b += static_cast<size_t>(pool_cap) * 4 + 2 * (pool_cap / 32) * 4;
+    b += (2 * k + kPassThreads) * 8 + (2 * k + kPassThreads) * 4 + 2 * k;
+    return b;
+}
+
+uint32_t pool_capacity(uint64_t n, uint32_t k) {
+    const uint64_t worst = std::min<uint64_t>(n, 4ull * k * k + k);
+    uint32_t cap = kPassThreads;
+    while (cap < 2 * worst) cap <<= 1;
+    return cap;
+}
+
+// Host-side partial Fisher-Yates (knn_graph.cpp:37-46) when 4k >= n.
+void sample_fisher_yates(uint64_t n, uint32_t k, uint64_t seed, std::vector<uint32_t>& ids) {
+    ids.resize(n * k);
+    std::vector<uint32_t> all;
+    for (uint64_t u = 0; u < n; ++u) {
+        SplitMix64 rng(mix_seed(seed, u));
+        all.clear();
+        for (uint32_t i = 0; i < n; ++i)
+            if (i != u) all.push_back(i);
+        for (uint32_t i = 0; i < k; ++i) {
+            const auto j = i + static_cast<uint32_t>(bounded(rng, all.size() - i));
+            std::swap(all[i], all[j]);
+            ids[u * k + i] = all[i];
+        }
+    }
+}
+
+}  // namespace
+
+void knn_init_device(const fg_corpus& c, uint32_t k, uint64_t seed, DevKnn& g, cudaStream_t s) {
+    if (k == 0) throw Error("invalid-k", "neighbour count must be positive");
+    if (c.n < static_cast<uint64_t>(k) + 1)
+        throw Error("corpus-too-small", "need at least " + std::to_string(k + 1) +
+                                            " documents for k=" + std::to_string(k));
+    g.alloc(c.n, k);
+    if (static_cast<uint64_t>(k) * 4 < c.n) {
+        knn_sample_kernel<<<(unsigned)((c.n + 255) / 256), 256, 0, s>>>(c.n, k, seed, g.ids.get());
+        FGB_LAUNCH("knn_sample_kernel");
+    } else {
+        std::vector<uint32_t> ids;
+        sample_fisher_yates(c.n, k, seed, ids);
+        g.ids.upload(ids, s);
+    }
+    const uint32_t lcap = hash_capacity(c.max_lnnz), scap = hash_capacity(c.max_snnz);
+    const size_t sm = doc_stage_bytes(c.dstride, lcap, scap) + static_cast<size_t>(k) * 12 + 16;
+    FGB_CUDA(cudaFuncSetAttribute(knn_init_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sm));
+    knn_init_score_kernel<<<(unsigned)c.n, std::min<uint32_t>(256, ((k + 31) / 32) * 32), sm, s>>>(
+        c.dc, k, g.ids.get(), g.scores.get(), g.fresh.get(), lcap, scap);
+    FGB_LAUNCH("knn_init_score_kernel");
+}
+
+uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
+    const uint64_t n = g.n;
+    const uint32_t k = g.k;
+    const uint64_t m = n * k;
+    if (m >= 0xFFFFFFFFull) throw Error("invalid-argument", "n*k exceeds 2^32 entries");
+
+    // ---- reverse lists (knn_graph.cpp:78-89)
+    DevBuf<uint64_t> keys_a(m), keys_b(m);
+    DevBuf<uint32_t> vals_a(m), vals_b(m), tkeys_a(m), tkeys_b(m), cnt(n), start(n);
+    DevBuf<uint32_t> rids(m), rcnt(n);
+    DevBuf<uint8_t> rfresh(m);
+    cnt.zero(s);
+    const unsigned gb = (unsigned)((m + 255) / 256);
+    score_keys_kernel<<<gb, 256, 0, s>>>(g.scores.get(), m, keys_a.get(), vals_a.get());
+    FGB_LAUNCH("score_keys_kernel");
+    size_t tb1 = 0, tb2 = 0, tb3 = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb1, keys_a.get(), keys_b.get(), vals_a.get(),
+                                              vals_b.get(), (int)m, 0, 64, s);
+    int bits = 1;
+    while ((1ull << bits) < n) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkeys_a.get(), tkeys_b.get(), vals_b.get(),
+                                    vals_a.get(), (int)m, 0, bits, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb3, cnt.get(), start.get(), (int)n, s);
+    DevBuf<unsigned char> temp(std::max({tb1, tb2, tb3, size_t(16)}));
+    size_t tb = temp.size();
+    FGB_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp.get(), tb, keys_a.get(), keys_b.get(),
+                                                       vals_a.get(), vals_b.get(), (int)m, 0, 64, s));
+    target_keys_kernel<<<gb, 256, 0, s>>>(g.ids.get(), vals_b.get(), m, tkeys_a.get(), cnt.get());
+    FGB_LAUNCH("target_keys_kernel");
+    tb = temp.size();
+    FGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tb, tkeys_a.get(), tkeys_b.get(),
+                                             vals_b.get(), vals_a.get(), (int)m, 0, bits, s));
+    tb = temp.size();
+    FGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.get(), tb, cnt.get(), start.get(), (int)n, s));
+    reverse_fill_kernel<<<gb, 256, 0, s>>>(n, k, vals_a.get(), cnt.get(), start.get(),
+                                           g.fresh.get(), rids.get(), rfresh.get(), rcnt.get());
+    FGB_LAUNCH("reverse_fill_kernel");
+    keys_a.release();
+    keys_b.release();
+    vals_b.release();
+    tkeys_a.release();
+    tkeys_b.release();
+    temp.release();
+
+    // ---- per-node two-hop join (knn_graph.cpp:91-142)
+    DevKnn next;
+    next.alloc(n, k);
+    DevBuf<unsigned long long> changed(1);
+    changed.zero(s);
+    const uint32_t lcap = hash_capacity(c.max_lnnz), scap = hash_capacity(c.max_snnz);
+    PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
+               rids.get(),     rfresh.get(), rcnt.get(),   next.ids.get(), next.scores.get(),
+               next.fresh.get(), changed.get(), pool_capacity(n, k), lcap, scap};
+    const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap);
+    if (sm > 227 * 1024)
+        throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
+                                            std::to_string(sm) + " B)");
+    FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    knn_pass_kernel<<<(unsigned)n, kPassThreads, sm, s>>>(a);
+    FGB_LAUNCH("knn_pass_kernel");
+    unsigned long long h_changed = 0;
+    changed.download(&h_changed, 1, s);
+    FGB_CUDA(cudaStreamSynchronize(s));
+    g.ids = std::move(next.ids);
+    g.scores = std::move(next.scores);
+    g.fresh = std::move(next.fresh);
+    return h_changed;
+}
+
+uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
+                          double convergence, uint64_t seed, DevKnn& g, cudaStream_t s) {
+    uint32_t k = k_req;
+    if (c.n >= 2 && k >= c.n) k = static_cast<uint32_t>(c.n - 1);  // knn_graph.cpp:153-156
+    knn_init_device(c, k, seed, g, s);
+    const double denom = static_cast<double>(c.n) * k;
+    uint32_t passes = 0;
+    for (uint32_t it = 0; it < max_iterations; ++it) {
+        const uint64_t changed = knn_iterate_device(c, g, s);
+        ++passes;
+        if (static_cast<double>(changed) / denom < convergence) break;
+    }
+    return passes;
+}
+
+}  // namespace fgb
+
+using namespace fgb;
+
+namespace {
+void lists_to_host(const DevKnn& g, fg_knn_lists* out, cudaStream_t s) {
+    out->k = g.k;
+    g.ids.download(out->ids, g.n * g.k, s);
+    g.scores.download(out->scores, g.n * g.k, s);
+    g.fresh.download(out->fresh, g.n * g.k, s);
+    FGB_CUDA(cudaStreamSynchronize(s));
+}
+void lists_to_device(const fg_knn_lists* in, DevKnn& g, cudaStream_t s) {
+    g.alloc(in->n, in->k);
+    g.ids.upload(in->ids, in->n * in->k, s);
+    g.scores.upload(in->scores, in->n * in->k, s);
+    g.fresh.upload(in->fresh, in->n * in->k, s);
+}
+}  // namespace
+
+extern "C" {
+
+int fg_knn_init(const fg_corpus* c, uint32_t k, uint64_t seed, fg_knn_lists* out) {
+    return guarded([&] {
+        if (!c || !out) throw Error("invalid-argument", "null pointer");
+        FGB_CUDA(cudaSetDevice(c->device));
+        DevKnn g;
+        knn_init_device(*c, k, seed, g, c->stream);
+        lists_to_host(g, out, c->stream);
+    });
+}
+
+int fg_knn_iterate(const fg_corpus* c, fg_knn_lists* lists, uint64_t* changed) {
+    return guarded([&] {
+        if (!c || !lists) throw Error("invalid-argument", "null pointer");
+        if (lists->n != c->n) throw Error("invalid-argument", "list count differs from corpus");
+        FGB_CUDA(cudaSetDevice(c->device));
+        DevKnn g;
+        lists_to_device(lists, g, c->stream);
+        const uint64_t ch = knn_iterate_device(*c, g, c->stream);
+        lists_to_host(g, lists, c->stream);
+        if (changed) *changed = ch;
+    });
+}
+
+int fg_knn_build(const fg_corpus* c, const fg_knn_params* p, fg_knn_lists* out, uint32_t* passes) {
+    return guarded([&] {
+        if (!c || !p || !out) throw Error("invalid-argument", "null pointer");
+        FGB_CUDA(cudaSetDevice(c->device));
+        DevKnn g;
+        const uint32_t ps = knn_build_device(*c, p->k, p->max_iterations, p->convergence, p->seed, g,
+                                             c->stream);
+        out->n = c->n;
+        lists_to_host(g, out, c->stream);
+        if (passes) *passes = ps;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// knn.cuh — device-resident NN-Descent state shared by knn.cu / index.
+#pragma once
+
+#include "fg_cuda.hpp"
+
+namespace fgb {
+
+// KnnGraph on the device: row u = k entries sorted by (score desc, id asc).
+struct DevKnn {
+    uint64_t n = 0;
+    uint32_t k = 0;
+    DevBuf<uint32_t> ids;
+    DevBuf<double> scores;
+    DevBuf<uint8_t> fresh;
+    void alloc(uint64_t n_, uint32_t k_) {
+        n = n_;
+        k = k_;
+        ids.alloc(n * k);
+        scores.alloc(n * k);
+        fresh.alloc(n * k);
+    }
+};
+
+// init_random_graph (knn_graph.cpp:52-73) into g (allocated n x k).
+void knn_init_device(const fg_corpus& c, uint32_t k, uint64_t seed, DevKnn& g, cudaStream_t s);
+// nn_descent_iterate (knn_graph.cpp:75-148), in place; returns #replaced.
+uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s);
+// build_knn_graph (knn_graph.cpp:150-166); returns the number of passes run.
+uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
+                          double convergence, uint64_t seed, DevKnn& g, cudaStream_t s);
+
+struct RefineOut {
+    uint32_t degree = 0, k = 0;
+    DevBuf<uint32_t> semantic;   // n x degree
+    DevBuf<uint32_t> keyword;    // n x k (recycled, reach order)
+    DevBuf<uint32_t> kw_count;   // n
+    DevBuf<uint32_t> ordered;    // n x k ranked candidate ids
+    DevBuf<double> ordered_sc;   // n x k
+    DevBuf<uint32_t> detours;    // n x k
+    DevBuf<uint32_t> kept;       // n x degree
+    DevBuf<uint32_t> kept_count; // n
+};
+
+// refine_graph (refine.cpp:167-217).
+void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool per_neighbour,
+                   RefineOut& out, cudaStream_t s);
+
+}  // namespace fgb

@@ -1,0 +1,477 @@
+// refine.cu — K4: the edge refinery on the GPU (refine.cpp:11-217).
+//
+// refine_node_kernel, one CTA per node u:
+//   * candidate Gram: every pair (i<j) of u's k candidates is scored
+//     bit-exactly (candidate_pair_scores, refine.cpp:11-23).  The dense part
+//     is a tiled SIMT "GEMM" whose every output keeps its sequential k-order
+//     (each thread owns whole dot products; the candidates' dense rows stream
+//     through shared memory in 64-float chunks), the sparse parts a merge-join;
+//   * detour counts, strict `<` (refine.cpp:25-39), and the rank sort by
+//     (detours asc, score desc, id asc) (refine.cpp:41-65) — thread per
+//     candidate, rank by counting;
+//   * the IP prune walk with keyword recycling (refine.cpp:67-118) — one warp
+//     walks the ranked list in order; the "first kept pruner" is a ballot, and
+//     the union keyword coverage is a shared-memory hash of the kept set.
+// merge_reverse_edges (refine.cpp:123-163) then runs as two stable radix sorts
+// of the kept entries by (target, position, keeper) plus a warp per node, and
+// the keyword lists drop ids that ended up semantic (refine.cpp:203-215).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "fg_cuda.hpp"
+#include "knn.cuh"
+
+namespace fgb {
+namespace {
+
+constexpr int kRefineThreads = 256;
+constexpr uint32_t kTile = 64;        // dense floats per staged chunk
+constexpr uint32_t kTileStride = kTile + 1;
+constexpr int kMaxPairsPerThread = 8;
+
+__device__ double merge_dot(const uint32_t* idx, const float* val, uint64_t oa, uint32_t na,
+                            uint64_t ob, uint32_t nb) {
+    double acc = 0.0;
+    uint32_t i = 0, j = 0;
+    while (i < na && j < nb) {
+        const uint32_t a = idx[oa + i], b = idx[ob + j];
+        if (a < b) {
+            ++i;
+        } else if (b < a) {
+            ++j;
+        } else {
+            acc = __fma_rn((double)val[oa + i], (double)val[ob + j], acc);
+            ++i;
+            ++j;
+        }
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void pair_of(uint32_t p, uint32_t k, uint32_t& i, uint32_t& j) {
+    // p enumerates (i, j), i < j, row by row
+    i = 0;
+    uint32_t rem = p;
+    while (rem >= k - 1 - i) {
+        rem -= k - 1 - i;
+        ++i;
+    }
+    j = i + 1 + rem;
+}
+
+struct RefineArgs {
+    DevCorpus c;
+    uint32_t k, degree;
+    int per_neighbour;
+    const uint32_t* L_ids;
+    const double* L_sc;
+    uint32_t* ordered;     // n x k
+    double* ordered_sc;    // n x k
+    uint32_t* detours;     // n x k
+    uint32_t* kept;        // n x degree
+    uint32_t* kept_count;  // n
+    uint32_t* recycled;    // n x k
+    uint32_t* rec_count;   // n
+    uint32_t kwcap;        // kept-keyword hash capacity (power of two)
+    uint32_t ukw_cap;      // max keyword list length
+};
+
+__global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t k = a.k;
+    const uint64_t u = blockIdx.x;
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    double* P = reinterpret_cast<double*>(smem);             // k*k
+    double* csc = P + k * k;                                 // k
+    float* tile = reinterpret_cast<float*>(csc + k);         // k * kTileStride
+    uint32_t* cid = reinterpret_cast<uint32_t*>(tile + k * kTileStride);
+    uint32_t* det = cid + k;
+    uint32_t* order = det + k;   // rank -> candidate index
+    uint32_t* kp = order + k;    // kept ranked positions
+    uint32_t* rec = kp + k;      // recycled ids
+    uint32_t* kwset = rec + k;   // kept-keyword hash
+    uint32_t* ukw = kwset + a.kwcap;
+    __shared__ uint32_t nkept, nrec;
+
+    for (uint32_t j = tid; j < k; j += nt) {
+        cid[j] = a.L_ids[u * k + j];
+        csc[j] = a.L_sc[u * k + j];
+        P[j * k + j] = 0.0;
+    }
+    for (uint32_t j = tid; j < a.kwcap; j += nt) kwset[j] = kEmpty;
+    const uint64_t ub = a.c.kw_ptr[u], ue = a.c.kw_ptr[u + 1];
+    const uint32_t nukw = static_cast<uint32_t>(ue - ub);
+    for (uint32_t j = tid; j < nukw; j += nt) ukw[j] = a.c.kw_idx[ub + j];
+    __syncthreads();
+
+    // ---- candidate Gram (refine.cpp:11-23)
+    const uint32_t npairs = k * (k - 1) / 2;
+    for (uint32_t pbase = 0; pbase < npairs; pbase += nt * kMaxPairsPerThread) {
+        double acc[kMaxPairsPerThread];
+        uint32_t pi[kMaxPairsPerThread], pj[kMaxPairsPerThread];
+#pragma unroll
+        for (int q = 0; q < kMaxPairsPerThread; ++q) {
+            acc[q] = 0.0;
+            const uint32_t p = pbase + q * nt + tid;
+            if (p < npairs) {
+                pair_of(p, k, pi[q], pj[q]);
+            } else {
+                pi[q] = pj[q] = 0xFFFFFFFFu;
+            }
+        }
+        for (uint32_t d0 = 0; d0 < a.c.dstride; d0 += kTile) {
+            const uint32_t w = min(kTile, a.c.dstride - d0);
+            for (uint32_t e = tid; e < k * w; e += nt) {
+                const uint32_t r = e / w, col = e % w;
+                tile[r * kTileStride + col] = a.c.dense[(uint64_t)cid[r] * a.c.dstride + d0 + col];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < kMaxPairsPerThread; ++q) {
+                if (pi[q] == 0xFFFFFFFFu) continue;
+                const float* ri = tile + pi[q] * kTileStride;
+                const float* rj = tile + pj[q] * kTileStride;
+                double s = acc[q];
+                for (uint32_t dd = 0; dd < w; ++dd) s = __fma_rn((double)ri[dd], (double)rj[dd], s);
+                acc[q] = s;
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < kMaxPairsPerThread; ++q) {
+            if (pi[q] == 0xFFFFFFFFu) continue;
+            const uint64_t x = cid[pi[q]], y = cid[pj[q]];
+            double s = acc[q];
+            s = __dadd_rn(s, merge_dot(a.c.l_idx, a.c.l_val, a.c.l_off[x], a.c.l_nnz[x], a.c.l_off[y], a.c.l_nnz[y]));
+            s = __dadd_rn(s, merge_dot(a.c.s_idx, a.c.s_val, a.c.s_off[x], a.c.s_nnz[x], a.c.s_off[y], a.c.s_nnz[y]));
+            P[pi[q] * k + pj[q]] = s;
+            P[pj[q] * k + pi[q]] = s;
+        }
+    }
+    __syncthreads();
+
+    // ---- detours (strict <) and rank (refine.cpp:25-65)
+    for (uint32_t v = tid; v < k; v += nt) {
+        const double dis_uv = -csc[v];
+        uint32_t cnt = 0;
+        for (uint32_t x = 0; x < k; ++x) {
+            if (x == v) continue;
+            const double dis_ux = -csc[x];
+            const double dis_xv = -P[x * k + v];
+            cnt += fmax(dis_ux, dis_xv) < dis_uv;
+        }
+        det[v] = cnt;
+    }
+    __syncthreads();
+    for (uint32_t v = tid; v < k; v += nt) {
+        uint32_t r = 0;
+        for (uint32_t w = 0; w < k; ++w) {
+            const bool before = det[w] != det[v]   ? det[w] < det[v]
+                                : csc[w] != csc[v] ? csc[w] > csc[v]
+                                                   : cid[w] < cid[v];
+            r += before;
+        }
+        order[r] = v;
+    }
+    __syncthreads();
+    for (uint32_t r = tid; r < k; r += nt) {
+        const uint32_t v = order[r];
+        a.ordered[u * k + r] = cid[v];
+        a.ordered_sc[u * k + r] = csc[v];
+        a.detours[u * k + r] = det[v];
+    }
+
+    // ---- IP prune walk + keyword recycling (refine.cpp:67-118), one warp
+    if (warp == 0) {
+        const uint32_t kwmask = a.kwcap - 1;
+        auto kw_insert = [&](uint32_t node) {
+            const uint64_t b = a.c.kw_ptr[node], e = a.c.kw_ptr[node + 1];
+            for (uint64_t t = b + lane; t < e; t += 32) {
+                const uint32_t key = a.c.kw_idx[t];
+                uint32_t s = hslot(key, kwmask);
+                while (true) {
+                    const uint32_t prev = atomicCAS(&kwset[s], kEmpty, key);
+                    if (prev == kEmpty || prev == key) break;
+                    s = (s + 1) & kwmask;
+                }
+            }
+            __syncwarp();
+        };
+        auto kw_has = [&](uint32_t key) {
+            uint32_t s = hslot(key, kwmask);
+            while (true) {
+                const uint32_t kk = kwset[s];
+                if (kk == key) return true;
+                if (kk == kEmpty) return false;
+                s = (s + 1) & kwmask;
+            }
+        };
+        uint32_t nk = 0, nr = 0;
+        if (k > 0) {
+            if (lane == 0) kp[0] = 0;
+            nk = 1;
+            __syncwarp();
+            kw_insert(cid[order[0]]);
+        }
+        for (uint32_t r = 1; r < k; ++r) {
+            const uint32_t v = order[r];
+            const uint32_t vid = cid[v];
+            const double self_ip = a.c.sqnorm[vid];
+            int pruner = -1;  // index into kp
+            for (uint32_t b = 0; b < nk && pruner < 0; b += 32) {
+                const uint32_t i = b + lane;
+                const bool hit = i < nk && P[order[kp[i]] * k + v] >= self_ip;
+                const uint32_t m = __ballot_sync(0xFFFFFFFFu, hit);
+                if (m) pruner = static_cast<int>(b + __ffs(m) - 1);
+            }
+            if (pruner < 0 && nk < a.degree) {
+                if (lane == 0) kp[nk] = r;
+                ++nk;
+                __syncwarp();
+                kw_insert(vid);
+                continue;
+            }
+            // dropped: recycle when shared keywords are not covered
+            const uint64_t vb = a.c.kw_ptr[vid], ve = a.c.kw_ptr[vid + 1];
+            const bool per = a.per_neighbour && pruner >= 0;
+            uint64_t pb = 0, pe = 0;
+            if (per) {
+                const uint32_t pid = cid[order[kp[pruner]]];
+                pb = a.c.kw_ptr[pid];
+                pe = a.c.kw_ptr[pid + 1];
+            }
+            bool any_shared = false, uncovered = false;
+            for (uint64_t t = vb + lane; t < ve; t += 32) {
+                const uint32_t key = a.c.kw_idx[t];
+                // sorted_intersection(node_kw, doc_kw) membership
+                uint32_t lo = 0, hi = nukw;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (ukw[mid] < key)
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                if (lo < nukw && ukw[lo] == key) {
+                    any_shared = true;
+                    const bool cov = per ? sorted_contains(a.c.kw_idx, pb, pe, key) : kw_has(key);
+                    uncovered |= !cov;
+                }
+            }
+            any_shared = __any_sync(0xFFFFFFFFu, any_shared);
+            uncovered = __any_sync(0xFFFFFFFFu, uncovered);
+            if (any_shared && uncovered) {
+                if (lane == 0) rec[nr] = vid;
+                ++nr;
+            }
+        }
+        __syncwarp();
+        for (uint32_t i = lane; i < nk; i += 32) a.kept[u * a.degree + i] = cid[order[kp[i]]];
+        for (uint32_t i = lane; i < nr; i += 32) a.recycled[u * k + i] = rec[i];
+        if (lane == 0) {
+            a.kept_count[u] = nk;
+            a.rec_count[u] = nr;
+        }
+    }
+}
+
+// (position, keeper) entries of every kept edge, keyed for the stable sorts.
+__global__ void keeper_keys_kernel(uint64_t n, uint32_t degree, const uint32_t* kept,
+                                   const uint32_t* kept_count, uint32_t* pos_key,
+                                   uint32_t* vals, uint32_t* cnt) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n * degree) return;
+    const uint64_t w = t / degree;
+    const uint32_t p = static_cast<uint32_t>(t % degree);
+    vals[t] = static_cast<uint32_t>(t);
+    if (p < kept_count[w]) {
+        pos_key[t] = p;
+        atomicAdd(&cnt[kept[t]], 1u);
+    } else {
+        pos_key[t] = 0xFFFFFFFFu;  // invalid: sorts last
+    }
+}
+
+__global__ void target_key_kernel(uint64_t n, uint32_t degree, const uint32_t* kept,
+                                  const uint32_t* kept_count, const uint32_t* order,
+                                  uint32_t* tkey) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= n * degree) return;
+    const uint32_t e = order[t];
+    const uint64_t w = e / degree;
+    const uint32_t p = e % degree;
+    tkey[t] = p < kept_count[w] ? kept[e] : static_cast<uint32_t>(n);
+}
+
+// merge_reverse_edges for node u (warp per node) + keyword disjointness.
+__global__ void merge_reverse_kernel(uint64_t n, uint32_t k, uint32_t degree, const uint32_t* kept,
+                                     const uint32_t* kept_count, const uint32_t* keepers,
+                                     const uint32_t* kstart, const uint32_t* kcnt,
+                                     const uint32_t* ordered, uint32_t* semantic,
+                                     uint32_t* recycled, uint32_t* rec_count) {
+    extern __shared__ uint32_t lists[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t u = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp;
+    if (u >= n) return;
+    uint32_t* list = lists + warp * degree;
+    const uint32_t half = degree / 2;
+    const uint32_t kc = kept_count[u];
+    const uint32_t fwd = min(half, kc);
+    for (uint32_t i = lane; i < fwd; i += 32) list[i] = kept[u * degree + i];
+    uint32_t size = fwd;
+    __syncwarp();
+    auto has = [&](uint32_t id) {
+        bool hit = false;
+        for (uint32_t i = lane; i < size; i += 32) hit |= list[i] == id;
+        return __any_sync(0xFFFFFFFFu, hit);
+    };
+    auto push = [&](uint32_t id) {
+        if (lane == 0) list[size] = id;
+        ++size;
+        __syncwarp();
+    };
+    const uint32_t rb = kstart[u], rn = kcnt[u];
+    for (uint32_t i = 0; i < rn; ++i) {
+        if (size >= fwd + half) break;
+        const uint32_t e = keepers[rb + i];
+        const uint32_t w = e / degree;
+        if (!has(w)) push(w);
+    }
+    for (uint32_t i = fwd; i < kc && size < degree; ++i) {
+        const uint32_t id = kept[u * degree + i];
+        if (!has(id)) push(id);
+    }
+    for (uint32_t i = 0; i < k && size < degree; ++i) {
+        const uint32_t id = ordered[u * k + i];
+        if (!has(id)) push(id);
+    }
+    for (uint32_t i = lane; i < size; i += 32) semantic[u * degree + i] = list[i];
+    // keyword lists stay disjoint from the semantic list (refine.cpp:207-215)
+    const uint32_t nr = rec_count[u];
+    uint32_t out = 0;
+    for (uint32_t i = 0; i < nr; ++i) {
+        const uint32_t id = recycled[u * k + i];
+        if (!has(id)) {
+            if (lane == 0) recycled[u * k + out] = id;
+            ++out;
+        }
+    }
+    if (lane == 0) rec_count[u] = out;
+}
+
+}  // namespace
+
+void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool per_neighbour,
+                   RefineOut& out, cudaStream_t s) {
+    const uint64_t n = g.n;
+    const uint32_t k = g.k;
+    if (degree == 0) throw Error("invalid-k", "degree must be positive");
+    if (k < 2) throw Error("invalid-k", "refinery needs at least two candidates");
+    if (static_cast<uint64_t>(k) * (k - 1) / 2 > static_cast<uint64_t>(kRefineThreads) * kMaxPairsPerThread * 64)
+        throw Error("invalid-k", "knn_k too large for the refinery kernel");
+    out.degree = degree;
+    out.k = k;
+    out.semantic.alloc(n * degree);
+    out.keyword.alloc(n * k);
+    out.kw_count.alloc(n);
+    out.ordered.alloc(n * k);
+    out.ordered_sc.alloc(n * k);
+    out.detours.alloc(n * k);
+    out.kept.alloc(n * degree);
+    out.kept_count.alloc(n);
+    FGB_CUDA(cudaMemsetAsync(out.semantic.get(), 0xFF, n * degree * 4, s));
+
+    uint32_t max_kw = 0;
+    for (size_t i = 0; i < c.keywords.rows(); ++i)
+        max_kw = std::max<uint32_t>(max_kw, static_cast<uint32_t>(c.keywords.len(i)));
+    uint32_t kwcap = 32;
+    while (kwcap < 2ull * max_kw * std::min(degree, k)) kwcap <<= 1;
+    RefineArgs a{c.dc, k, degree, per_neighbour ? 1 : 0, g.ids.get(), g.scores.get(),
+                 out.ordered.get(), out.ordered_sc.get(), out.detours.get(), out.kept.get(),
+                 out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw};
+    const size_t sm = static_cast<size_t>(k) * k * 8 + k * 8 + static_cast<size_t>(k) * kTileStride * 4 +
+                      5 * k * 4 + static_cast<size_t>(kwcap) * 4 + static_cast<size_t>(max_kw) * 4 + 16;
+    if (sm > 227 * 1024)
+        throw Error("invalid-k", "refinery shared memory exceeds the SM (" + std::to_string(sm) + " B)");
+    FGB_CUDA(cudaFuncSetAttribute(refine_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    refine_node_kernel<<<(unsigned)n, kRefineThreads, sm, s>>>(a);
+    FGB_LAUNCH("refine_node_kernel");
+
+    // ---- keepers sorted by (target, position, keeper) (refine.cpp:127-133)
+    const uint64_t m = n * degree;
+    DevBuf<uint32_t> pos_a(m), pos_b(m), vals_a(m), vals_b(m), tkey_a(m), tkey_b(m), cnt(n + 1),
+        start(n + 1);
+    cnt.zero(s);
+    const unsigned gb = (unsigned)((m + 255) / 256);
+    keeper_keys_kernel<<<gb, 256, 0, s>>>(n, degree, out.kept.get(), out.kept_count.get(),
+                                          pos_a.get(), vals_a.get(), cnt.get());
+    FGB_LAUNCH("keeper_keys_kernel");
+    int tbits = 1;
+    while ((1ull << tbits) <= n) ++tbits;
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, pos_a.get(), pos_b.get(), vals_a.get(), vals_b.get(), (int)m, 0, 32, s);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, tkey_a.get(), tkey_b.get(), vals_b.get(), vals_a.get(), (int)m, 0, tbits, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, cnt.get(), start.get(), (int)n, s);
+    DevBuf<unsigned char> temp(std::max({t1, t2, t3, size_t(16)}));
+    size_t tb = temp.size();
+    FGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tb, pos_a.get(), pos_b.get(), vals_a.get(),
+                                             vals_b.get(), (int)m, 0, 32, s));
+    target_key_kernel<<<gb, 256, 0, s>>>(n, degree, out.kept.get(), out.kept_count.get(),
+                                         vals_b.get(), tkey_a.get());
+    FGB_LAUNCH("target_key_kernel");
+    tb = temp.size();
+    FGB_CUDA(cub::DeviceRadixSort::SortPairs(temp.get(), tb, tkey_a.get(), tkey_b.get(), vals_b.get(),
+                                             vals_a.get(), (int)m, 0, tbits, s));
+    tb = temp.size();
+    FGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.get(), tb, cnt.get(), start.get(), (int)n, s));
+    const int warps = 8;
+    merge_reverse_kernel<<<(unsigned)((n + warps - 1) / warps), warps * 32, warps * degree * 4, s>>>(
+        n, k, degree, out.kept.get(), out.kept_count.get(), vals_a.get(), start.get(), cnt.get(),
+        out.ordered.get(), out.semantic.get(), out.keyword.get(), out.kw_count.get());
+    FGB_LAUNCH("merge_reverse_kernel");
+    FGB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace fgb
+
+using namespace fgb;
+
+extern "C" {
+
+int fg_refine(const fg_corpus* c, const fg_knn_lists* knn, const fg_refine_params* p,
+              fg_refined* out, fg_refine_trace* trace) {
+    return guarded([&] {
+        if (!c || !knn || !p || !out) throw Error("invalid-argument", "null pointer");
+        if (knn->n != c->n) throw Error("invalid-argument", "list count differs from corpus");
+        if (out->keyword_cap < knn->k) throw Error("invalid-argument", "keyword_cap < k");
+        FGB_CUDA(cudaSetDevice(c->device));
+        cudaStream_t s = c->stream;
+        DevKnn g;
+        g.alloc(knn->n, knn->k);
+        g.ids.upload(knn->ids, knn->n * knn->k, s);
+        g.scores.upload(knn->scores, knn->n * knn->k, s);
+        g.fresh.upload(knn->fresh, knn->n * knn->k, s);
+        RefineOut r;
+        refine_device(*c, g, p->degree, p->per_neighbour_keyword_check != 0, r, s);
+        const uint64_t n = knn->n;
+        const uint32_t k = knn->k;
+        r.semantic.download(out->semantic, n * p->degree, s);
+        std::vector<uint32_t> kw(n * k);
+        r.keyword.download(kw.data(), n * k, s);
+        r.kw_count.download(out->keyword_count, n, s);
+        if (trace) {
+            if (trace->ordered_ids) r.ordered.download(trace->ordered_ids, n * k, s);
+            if (trace->ordered_scores) r.ordered_sc.download(trace->ordered_scores, n * k, s);
+            if (trace->detours) r.detours.download(trace->detours, n * k, s);
+            if (trace->kept) r.kept.download(trace->kept, n * p->degree, s);
+            if (trace->kept_count) r.kept_count.download(trace->kept_count, n, s);
+        }
+        FGB_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t u = 0; u < n; ++u)
+            std::copy(kw.begin() + u * k, kw.begin() + u * k + out->keyword_count[u],
+                      out->keyword + u * out->keyword_cap);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1047 @@
+// search.cu — K5: batched beam search (search.cpp:141-293) on the GPU.
+//
+// One WARP owns one query at a time (persistent warps pull query ids from a
+// global counter).  Per-query state lives in that warp's slice of shared
+// memory: the staged weighted query (dense + sparse hashes), the sorted
+// `cand` beam and `topk` pools, and the current expansion's neighbour list.
+// Visited ("scored") flags are an exact per-warp bitset in HBM (n bits,
+// cleared through a touched list), so no per-query O(n) state is allocated.
+//
+// Exactness.  Scores are bit-identical to the reference (device_common.cuh).
+// The best-first order is the reference's: expand the first unexpanded
+// cand entry; neighbours in reach order (semantic, keyword if u shares a
+// required keyword, logical vias of group ent(u) while hop < max hops).
+//  * Plain queries (no entity context possible): a re-offer of an already
+//    scored node is a no-op in Pool::offer (its distance never changes and
+//    the pool's worst entry only improves), so only first-time neighbours are
+//    offered; the cand pool content is offer-order independent
+//    (search.cpp:22-24), so they merge as one sorted batch.  topk merges as a
+//    batch too unless required keywords make the twin pool order-dependent,
+//    in which case lane 0 replays the offers in reach order (search.cpp:171-181).
+//  * Entity-context queries: context propagation runs first for the whole
+//    neighbour list in reach order (it depends only on u's context and each
+//    neighbour's own state), then every neighbour whose adjusted distance is
+//    new or changed is offered in reach order with warp-cooperative
+//    single-entry offers (exactly Pool::offer, search.cpp:26-42).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "fg_cuda.hpp"
+#include "index.hpp"
+#include "query_stage.cuh"
+
+namespace fgb {
+namespace {
+
+constexpr uint32_t kFlagExp = 0x80000000u;  // cand entry expanded
+constexpr uint32_t kNodeMask = 0x7FFFFFFFu;
+constexpr int kWarpsPerBlock = 4;
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+enum : uint32_t { QF_VALID = 1, QF_ENTITY = 2, QF_FALLBACK = 4 };
+enum : uint32_t { ERR_TWIN = 1, ERR_CTX = 2 };
+
+struct SearchArgs {
+    DevCorpus c;
+    const uint32_t* semantic;
+    uint32_t degree;
+    const uint64_t* kw_ptr;
+    const uint32_t* kw_idx;
+    const uint64_t* lg_ptr;
+    const uint4* lg;
+    const uint64_t* kg_ptr;
+    const uint32_t* kg_nbr;
+    uint32_t kg_rows;
+    DevQueries q;
+    const uint64_t* seed_ptr;
+    const uint32_t* seed_node;
+    const uint32_t* seed_ent;
+    const uint8_t* seed_has;
+    const uint32_t* norm_order;
+    uint32_t entry_count;
+    const uint8_t* qflags;
+    int conjunctive;
+    uint32_t lcap, scap, beamcap, kcap, nbcap, lccap, reqcap;
+    uint32_t warp_smem;
+    uint32_t* visited;
+    uint32_t* expbits;
+    uint32_t* twinbits;
+    uint64_t nwords;
+    uint32_t* touched;
+    uint32_t tcap;
+    uint32_t* twin_node;
+    double* twin_raw;
+    uint32_t twcap;
+    uint4* ctx;
+    uint32_t ctxcap;
+    uint32_t hit_stride;
+    uint32_t* r_node;
+    double* r_score;
+    uint32_t* r_count;
+    unsigned long long* r_expanded;
+    unsigned long long* r_scored;
+    uint32_t* r_warn;
+    uint32_t* r_err;
+    unsigned int* work;
+};
+
+__device__ __forceinline__ bool eless(double d1, uint32_t n1, double d2, uint32_t n2) {
+    return d1 < d2 || (d1 == d2 && n1 < n2);  // entry_less (search.cpp:13-16)
+}
+
+// Per-warp shared-memory views.
+struct WarpMem {
+    unsigned char* stage;
+    double* cand_d;
+    uint32_t* cand_n;
+    double* topk_d;
+    double* topk_raw;
+    uint32_t* topk_n;
+    double* nd;       // dist per new node
+    uint32_t* nb;     // neighbour ids, reach order
+    uint32_t* nnew;   // positions (in nb) of first-time neighbours
+    uint8_t* nflag;   // per nb position: 1 new, 2 ctx changed
+    uint32_t* lc;     // (via, target) pairs of the logical group
+    uint32_t* req;    // required keywords (sorted)
+    double* bd;       // batch sort buffer
+    uint32_t* bn;
+};
+
+__device__ WarpMem carve(unsigned char* base, const SearchArgs& a) {
+    WarpMem m;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = base + off;
+        off += (bytes + 15) & ~size_t(15);
+        return p;
+    };
+    m.stage = take(static_cast<size_t>(a.c.dstride) * 4 + static_cast<size_t>(a.lcap + a.scap) * 8);
+    m.cand_d = reinterpret_cast<double*>(take(a.beamcap * 8));
+    m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
+    m.topk_raw = reinterpret_cast<double*>(take(a.kcap * 8));
+    m.nd = reinterpret_cast<double*>(take(a.nbcap * 8));
+    m.bd = reinterpret_cast<double*>(take(32 * 8));
+    m.cand_n = reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
+    m.topk_n = reinterpret_cast<uint32_t*>(take(a.kcap * 4));
+    m.nb = reinterpret_cast<uint32_t*>(take(a.nbcap * 4));
+    m.nnew = reinterpret_cast<uint32_t*>(take(a.nbcap * 4));
+    m.nflag = reinterpret_cast<uint8_t*>(take(a.nbcap));
+    m.lc = reinterpret_cast<uint32_t*>(take(a.lccap * 8 + 8));
+    m.req = reinterpret_cast<uint32_t*>(take(a.reqcap * 4 + 4));
+    m.bn = reinterpret_cast<uint32_t*>(take(32 * 4));
+    return m;
+}
+
+// ---------------------------------------------------------------- pools
+// Sorted pool (dist asc, node asc) in smem: warp-cooperative primitives.
+struct PoolRef {
+    double* d;
+    uint32_t* n;   // node | kFlagExp (cand) ; node (topk)
+    uint32_t cap;
+};
+
+__device__ __forceinline__ int pool_find(const PoolRef& p, uint32_t size, uint32_t node,
+                                         uint32_t lane) {
+    for (uint32_t b = 0; b < size; b += 32) {
+        const uint32_t i = b + lane;
+        const bool hit = i < size && (p.n[i] & kNodeMask) == node;
+        const uint32_t m = __ballot_sync(kFull, hit);
+        if (m) return static_cast<int>(b + __ffs(m) - 1);
+    }
+    return -1;
+}
+
+// # entries strictly less than (d, node) (== upper_bound with unique nodes).
+__device__ __forceinline__ uint32_t pool_rank(const PoolRef& p, uint32_t size, double d,
+                                              uint32_t node) {
+    uint32_t lo = 0, hi = size;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (eless(p.d[mid], p.n[mid] & kNodeMask, d, node))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Pool::offer (search.cpp:26-42), all lanes with uniform arguments.
+// Returns the evicted node or -1; `flag` is stored with the node.
+__device__ int64_t pool_offer(const PoolRef& p, uint32_t& size, double d, uint32_t node,
+                              uint32_t flag, uint32_t lane) {
+    const int pos = pool_find(p, size, node, lane);
+    if (pos >= 0) {
+        if (!eless(d, node, p.d[pos], node)) return -1;  // no improvement
+        flag = p.n[pos] & kFlagExp;
+        for (uint32_t b = pos + 1; b < size; b += 32) {  // erase: shift left
+            const uint32_t i = b + lane;
+            double dd = 0;
+            uint32_t nn = 0;
+            if (i < size) {
+                dd = p.d[i];
+                nn = p.n[i];
+            }
+            __syncwarp();
+            if (i < size) {
+                p.d[i - 1] = dd;
+                p.n[i - 1] = nn;
+            }
+            __syncwarp();
+        }
+        --size;
+    } else if (size == p.cap) {
+        if (!eless(d, node, p.d[size - 1], p.n[size - 1] & kNodeMask)) return -1;
+    }
+    const uint32_t ins = pool_rank(p, size, d, node);
+    int64_t evicted = -1;
+    if (size == p.cap) evicted = p.n[size - 1] & kNodeMask;
+    __syncwarp();
+    const uint32_t last = min(size, p.cap - 1);  // entries [ins, last) move right by one
+    if (last > ins) {
+        for (int b = static_cast<int>(((last - 1 - ins) / 32) * 32 + ins); b >= static_cast<int>(ins); b -= 32) {
+            const uint32_t i = b + lane;
+            double dd = 0;
+            uint32_t nn = 0;
+            const bool v = i < last;
+            if (v) {
+                dd = p.d[i];
+                nn = p.n[i];
+            }
+            __syncwarp();
+            if (v) {
+                p.d[i + 1] = dd;
+                p.n[i + 1] = nn;
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0) {
+        p.d[ins] = d;
+        p.n[ins] = node | flag;
+    }
+    __syncwarp();
+    if (size < p.cap) ++size;
+    return evicted;
+}
+
+// Batch merge of m <= 32 new entries (sorted, in bd/bn, all absent from the
+// pool) — the set result of offering them one by one.  Returns the smallest
+// insertion position (or cap when nothing entered).
+__device__ uint32_t pool_merge(const PoolRef& p, uint32_t& size, const double* bd,
+                               const uint32_t* bn, uint32_t m, uint32_t lane) {
+    if (m == 0) return p.cap;
+    uint32_t mypos = p.cap;
+    double md = 0;
+    uint32_t mn = 0;
+    if (lane < m) {
+        md = bd[lane];
+        mn = bn[lane];
+        mypos = lane + pool_rank(p, size, md, mn);
+    }
+    __syncwarp();
+    if (size > 0) {
+        for (int b = static_cast<int>(((size - 1) / 32) * 32); b >= 0; b -= 32) {
+            const uint32_t i = b + lane;
+            const bool v = i < size;
+            double dd = 0;
+            uint32_t nn = 0, np = p.cap;
+            if (v) {
+                dd = p.d[i];
+                nn = p.n[i];
+                uint32_t lo = 0, hi = m;  // # new entries < pool[i]
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (eless(bd[mid], bn[mid], dd, nn & kNodeMask))
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                np = i + lo;
+            }
+            __syncwarp();
+            if (v && np < p.cap) {
+                p.d[np] = dd;
+                p.n[np] = nn;
+            }
+            __syncwarp();
+        }
+    }
+    if (lane < m && mypos < p.cap) {
+        p.d[mypos] = md;
+        p.n[mypos] = mn;  // new entries are unexpanded
+    }
+    __syncwarp();
+    size = min(size + m, p.cap);
+    uint32_t mn_pos = mypos;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn_pos = min(mn_pos, __shfl_xor_sync(kFull, mn_pos, o));
+    return mn_pos;
+}
+
+// Warp bitonic sort of one (dist, node) pair per lane (invalid lanes carry +inf).
+__device__ __forceinline__ void warp_sort(double& d, uint32_t& n, uint32_t lane) {
+#pragma unroll
+    for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            const double od = __shfl_xor_sync(kFull, d, j);
+            const uint32_t on = __shfl_xor_sync(kFull, n, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            const bool other_less = eless(od, on, d, n);
+            const bool take = (lower == up) ? other_less : (!other_less && (od != d || on != n));
+            if (take) {
+                d = od;
+                n = on;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ bool bit_test_set(uint32_t* bits, uint32_t node) {
+    const uint32_t m = 1u << (node & 31);
+    return (atomicOr(&bits[node >> 5], m) & m) != 0;
+}
+__device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t node) {
+    return (bits[node >> 5] >> (node & 31)) & 1u;
+}
+
+// shares_required (search.cpp:163-167): u holds ANY required keyword.
+__device__ bool shares_required(const DevCorpus& c, uint32_t node, const uint32_t* req, uint32_t R,
+                                uint32_t lane) {
+    bool hit = false;
+    const uint64_t b = c.kw_ptr[node], e = c.kw_ptr[node + 1];
+    for (uint32_t i = lane; i < R; i += 32) hit |= sorted_contains(c.kw_idx, b, e, req[i]);
+    return __any_sync(kFull, hit);
+}
+
+// has_relation (types.cpp:52-57) on the device adjacency.
+__device__ bool has_relation(const SearchArgs& a, uint32_t x, uint32_t y) {
+    if (x >= a.kg_rows) return false;
+    return sorted_contains(a.kg_nbr, a.kg_ptr[x], a.kg_ptr[x + 1], y);
+}
+
+// Entity-context table (per warp, global memory): (node, ent, hop, has).
+__device__ int ctx_find(const uint4* t, uint32_t cap, uint32_t node) {
+    uint32_t s = hslot(node, cap - 1);
+    while (true) {
+        const uint4 e = t[s];
+        if (e.x == node) return static_cast<int>(s);
+        if (e.x == kEmpty) return -1;
+        s = (s + 1) & (cap - 1);
+    }
+}
+__device__ int ctx_slot(uint4* t, uint32_t cap, uint32_t node, uint32_t& used) {
+    uint32_t s = hslot(node, cap - 1);
+    while (true) {
+        const uint4 e = t[s];
+        if (e.x == node) return static_cast<int>(s);
+        if (e.x == kEmpty) {
+            t[s] = make_uint4(node, 0, 0, 0);
+            ++used;
+            return static_cast<int>(s);
+        }
+        s = (s + 1) & (cap - 1);
+    }
+}
+
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t slot = blockIdx.x * (uint64_t)kWarpsPerBlock + warp;
+    WarpMem w = carve(smem_raw + static_cast<size_t>(warp) * a.warp_smem, a);
+    uint32_t* visited = a.visited + slot * a.nwords;
+    uint32_t* expbits = a.expbits ? a.expbits + slot * a.nwords : nullptr;
+    uint32_t* twinbits = a.twinbits ? a.twinbits + slot * a.nwords : nullptr;
+    uint32_t* touched = a.touched + slot * a.tcap;
+    uint32_t* twin_node = a.twin_node ? a.twin_node + slot * a.twcap : nullptr;
+    double* twin_raw = a.twin_raw ? a.twin_raw + slot * a.twcap : nullptr;
+    uint4* ctx = a.ctx ? a.ctx + slot * a.ctxcap : nullptr;
+    const DevCorpus& c = a.c;
+
+    while (true) {
+        uint32_t qi = 0;
+        if (lane == 0) qi = atomicAdd(a.work, 1u);
+        qi = __shfl_sync(kFull, qi, 0);
+        if (qi >= a.q.count) break;
+        const uint32_t flags = a.qflags[qi];
+        if (!(flags & QF_VALID)) {
+            if (lane == 0) {
+                a.r_count[qi] = 0;
+                a.r_expanded[qi] = 0;
+                a.r_scored[qi] = 0;
+                a.r_warn[qi] = 0;
+                a.r_err[qi] = 0;
+            }
+            continue;
+        }
+        const uint32_t K = a.q.k[qi], B = a.q.beam[qi], H = a.q.hops[qi];
+        const double went = static_cast<double>(a.q.weights[qi].w);
+        const bool ctx_mode = (flags & QF_ENTITY) != 0;
+        SmemQuery sq;
+        stage_query(a.q, qi, c.dstride, w.stage, a.lcap, a.scap, lane, 32, sq, [] { __syncwarp(); });
+        const uint64_t rb = a.q.req_ptr[qi];
+        const uint32_t R = static_cast<uint32_t>(a.q.req_ptr[qi + 1] - rb);
+        for (uint32_t i = lane; i < R; i += 32) w.req[i] = a.q.req_idx[rb + i];
+        __syncwarp();
+
+        PoolRef cand{w.cand_d, w.cand_n, B};
+        PoolRef topk{w.topk_d, w.topk_n, K};
+        uint32_t csize = 0, tsize = 0, ntouched = 0, ntwin = 0, ctx_used = 0, err = 0;
+        unsigned long long expanded = 0, scored = 0;
+        bool tover = false;
+
+        // ---- helpers bound to this query -------------------------------
+        auto touch = [&](uint32_t node, bool mine) {  // record a visited node
+            const uint32_t m = __ballot_sync(kFull, mine);
+            const uint32_t pos = ntouched + __popc(m & ((1u << lane) - 1));
+            if (mine && pos < a.tcap) touched[pos] = node;
+            ntouched += __popc(m);
+        };
+        // topk offer by lane 0 in reach order, twin pool on eviction
+        auto topk_offer_seq = [&](uint32_t node, double dist, double raw) {
+            // (all lanes call; lane 0 does the work; state kept uniform via shfl)
+            int64_t ev = -1;
+            double ev_raw = 0;
+            if (lane == 0) {
+                int pos = -1;
+                for (uint32_t i = 0; i < tsize; ++i)
+                    if (w.topk_n[i] == node) pos = static_cast<int>(i);
+                bool go = true;
+                if (pos >= 0) {
+                    if (!eless(dist, node, w.topk_d[pos], node)) {
+                        go = false;
+                    } else {
+                        for (uint32_t i = pos + 1; i < tsize; ++i) {
+                            w.topk_d[i - 1] = w.topk_d[i];
+                            w.topk_n[i - 1] = w.topk_n[i];
+                            w.topk_raw[i - 1] = w.topk_raw[i];
+                        }
+                        --tsize;
+                    }
+                } else if (tsize == K && !eless(dist, node, w.topk_d[tsize - 1], w.topk_n[tsize - 1])) {
+                    go = false;
+                }
+                if (go) {
+                    uint32_t ins = 0;
+                    while (ins < tsize && !eless(dist, node, w.topk_d[ins], w.topk_n[ins])) ++ins;
+                    if (tsize == K) {
+                        ev = w.topk_n[tsize - 1];
+                        ev_raw = w.topk_raw[tsize - 1];
+                    }
+                    const uint32_t last = min(tsize, K - 1);
+                    for (int i = static_cast<int>(last) - 1; i >= static_cast<int>(ins); --i) {
+                        w.topk_d[i + 1] = w.topk_d[i];
+                        w.topk_n[i + 1] = w.topk_n[i];
+                        w.topk_raw[i + 1] = w.topk_raw[i];
+                    }
+                    w.topk_d[ins] = dist;
+                    w.topk_n[ins] = node;
+                    w.topk_raw[ins] = raw;
+                    if (tsize < K) ++tsize;
+                }
+            }
+            tsize = __shfl_sync(kFull, tsize, 0);
+            ev = __shfl_sync(kFull, ev, 0);
+            ev_raw = __shfl_sync(kFull, ev_raw, 0);
+            __syncwarp();
+            if (ev >= 0 && R > 0) {
+                const uint32_t e = static_cast<uint32_t>(ev);
+                if (!bit_test(twinbits, e) && shares_required(c, e, w.req, R, lane)) {
+                    if (lane == 0) {
+                        twinbits[e >> 5] |= 1u << (e & 31);
+                        if (ntwin < a.twcap) {
+                            twin_node[ntwin] = e;
+                            twin_raw[ntwin] = ev_raw;
+                        }
+                    }
+                    if (ntwin >= a.twcap) err |= ERR_TWIN;
+                    ++ntwin;
+                }
+            }
+        };
+        // adjusted distance (search.cpp:156-161)
+        auto adjusted = [&](double raw, uint32_t node) {
+            if (!ctx_mode) return raw;
+            const int s = ctx_find(ctx, a.ctxcap, node);
+            if (s >= 0) {
+                const uint4 e = ctx[s];
+                if (e.w && e.z >= 1) return raw - went / static_cast<double>(e.z);
+            }
+            return raw;
+        };
+        // assign_ctx (search.cpp:191-198), lane 0; returns true on change
+        auto assign_ctx = [&](uint32_t node, uint32_t ent, uint32_t hop) {
+            const int s = ctx_slot(ctx, a.ctxcap, node, ctx_used);
+            const uint4 e = ctx[s];
+            if (e.w && (e.z < hop || (e.z == hop && e.y <= ent))) return false;
+            ctx[s] = make_uint4(node, ent, hop, 1u);
+            return true;
+        };
+        // deleted nodes never reach topk (search.cpp:174)
+        auto is_deleted = [&](uint32_t node) { return c.deleted[node] != 0; };
+
+        // ---- seeds (search.cpp:205-216) --------------------------------
+        const bool norm_seeds = !(flags & QF_ENTITY);
+        const uint64_t sb = norm_seeds ? 0 : a.seed_ptr[qi];
+        const uint32_t nseeds = norm_seeds ? a.entry_count
+                                           : static_cast<uint32_t>(a.seed_ptr[qi + 1] - sb);
+        for (uint32_t base = 0; base < nseeds; base += 32) {
+            const uint32_t i = base + lane;
+            const bool v = i < nseeds;
+            uint32_t node = 0, ent = 0;
+            bool has = false;
+            double raw = 0;
+            if (v) {
+                node = norm_seeds ? a.norm_order[i] : a.seed_node[sb + i];
+                if (!norm_seeds) {
+                    ent = a.seed_ent[sb + i];
+                    has = a.seed_has[sb + i] != 0;
+                }
+                bit_test_set(visited, node);
+                raw = -hybrid_score(c, sq, node);
+            }
+            touch(node, v);
+            scored += __popc(__ballot_sync(kFull, v));
+            const uint32_t cnt = min(32u, nseeds - base);
+            for (uint32_t j = 0; j < cnt; ++j) {  // offers in seed order
+                const uint32_t nj = __shfl_sync(kFull, node, j);
+                const uint32_t ej = __shfl_sync(kFull, ent, j);
+                const bool hj = __shfl_sync(kFull, has, j);
+                const double rj = __shfl_sync(kFull, raw, j);
+                if (hj && lane == 0) assign_ctx(nj, ej, 0);
+                ctx_used = __shfl_sync(kFull, ctx_used, 0);
+                __syncwarp();
+                const double dj = adjusted(rj, nj);
+                pool_offer(cand, csize, dj, nj, 0, lane);
+                if (!is_deleted(nj)) topk_offer_seq(nj, dj, rj);
+            }
+        }
+        if (ctx_used * 2 > a.ctxcap) err |= ERR_CTX;
+
+        // ---- best-first expansion (search.cpp:218-264) ------------------
+        uint32_t cursor = 0;
+        while (err == 0) {
+            int upos = -1;
+            for (uint32_t b = cursor; b < csize && upos < 0; b += 32) {
+                const uint32_t i = b + lane;
+                const bool un = i < csize && !(w.cand_n[i] & kFlagExp);
+                const uint32_t m = __ballot_sync(kFull, un);
+                if (m) upos = static_cast<int>(b + __ffs(m) - 1);
+            }
+            if (upos < 0) break;
+            cursor = upos;
+            const uint32_t u = w.cand_n[upos] & kNodeMask;
+            if (lane == 0) {
+                w.cand_n[upos] |= kFlagExp;
+                if (expbits) expbits[u >> 5] |= 1u << (u & 31);
+            }
+            __syncwarp();
+            ++expanded;
+
+            // neighbours in reach order
+            uint32_t nbc = a.degree;
+            for (uint32_t j = lane; j < a.degree; j += 32) w.nb[j] = a.semantic[(uint64_t)u * a.degree + j];
+            if (R > 0 && shares_required(c, u, w.req, R, lane)) {
+                const uint64_t kb = a.kw_ptr[u], ke = a.kw_ptr[u + 1];
+                for (uint64_t j = kb + lane; j < ke; j += 32) w.nb[nbc + (j - kb)] = a.kw_idx[j];
+                nbc += static_cast<uint32_t>(ke - kb);
+            }
+            bool propagate = false;
+            uint32_t uent = 0, uhop = 0, nlc = 0;
+            if (ctx_mode) {
+                const int s = ctx_find(ctx, a.ctxcap, u);
+                if (s >= 0 && ctx[s].w) {
+                    uent = ctx[s].y;
+                    uhop = ctx[s].z;
+                    propagate = uhop < H;
+                }
+                if (propagate) {
+                    const uint64_t lb = a.lg_ptr[u], le = a.lg_ptr[u + 1];
+                    for (uint64_t j = lb; j < le; j += 32) {  // group source == ent(u)
+                        const uint64_t e = j + lane;
+                        uint4 ed = make_uint4(0, 0, 0, 0);
+                        const bool hit = e < le && (ed = a.lg[e]).x == uent;
+                        const uint32_t m = __ballot_sync(kFull, hit);
+                        const uint32_t pos = nlc + __popc(m & ((1u << lane) - 1));
+                        if (hit) {
+                            w.nb[nbc + pos] = ed.w;
+                            w.lc[2 * pos] = ed.w;
+                            w.lc[2 * pos + 1] = ed.z;
+                        }
+                        nlc += __popc(m);
+                    }
+                    nbc += nlc;
+                }
+            }
+            __syncwarp();
+
+            // dedupe (reach order) + first-time detection
+            uint32_t nnew = 0, nkeep = 0;
+            for (uint32_t b = 0; b < nbc; b += 32) {
+                const uint32_t i = b + lane;
+                const bool v = i < nbc;
+                const uint32_t x = v ? w.nb[i] : kEmpty;
+                bool keep = v;
+                if (v) {  // drop repeats of an earlier position
+                    for (uint32_t j = 0; j < i && keep; ++j) keep = w.nb[j] != x;
+                }
+                bool fresh = false;
+                if (keep) fresh = !bit_test_set(visited, x);
+                __syncwarp();
+                const uint32_t km = __ballot_sync(kFull, keep);
+                const uint32_t kpos = nkeep + __popc(km & ((1u << lane) - 1));
+                if (keep) {
+                    w.nb[kpos] = x;  // compact in place (kpos <= i)
+                    w.nflag[kpos] = fresh ? 1 : 0;
+                }
+                const uint32_t fm = __ballot_sync(kFull, fresh);
+                if (fresh) w.nnew[nnew + __popc(fm & ((1u << lane) - 1))] = kpos;
+                touch(x, fresh);
+                nkeep += __popc(km);
+                nnew += __popc(fm);
+                __syncwarp();
+            }
+            nbc = nkeep;
+            scored += nnew;
+
+            // score first-time neighbours, lane per node
+            for (uint32_t b = 0; b < nnew; b += 32) {
+                const uint32_t i = b + lane;
+                if (i < nnew) {
+                    const uint32_t pos = w.nnew[i];
+                    w.nd[pos] = -hybrid_score(c, sq, w.nb[pos]);
+                }
+            }
+            __syncwarp();
+
+            if (!ctx_mode) {
+                // cand: one sorted batch per 32 new nodes (order independent)
+                for (uint32_t b = 0; b < nnew; b += 32) {
+                    const uint32_t i = b + lane;
+                    double d = __longlong_as_double(0x7FF0000000000000ll);
+                    uint32_t nn = kEmpty;
+                    if (i < nnew) {
+                        nn = w.nb[w.nnew[i]];
+                        d = w.nd[w.nnew[i]];
+                    }
+                    warp_sort(d, nn, lane);
+                    w.bd[lane] = d;
+                    w.bn[lane] = nn;
+                    __syncwarp();
+                    const uint32_t m = min(32u, nnew - b);
+                    const uint32_t p0 = pool_merge(cand, csize, w.bd, w.bn, m, lane);
+                    cursor = min(cursor, p0);
+                    if (R == 0) {  // topk batch, deleted nodes skipped
+                        const bool ok = lane < m && !is_deleted(nn);
+                        const uint32_t om = __ballot_sync(kFull, ok);
+                        // keep sorted order among the survivors
+                        const uint32_t pos = __popc(om & ((1u << lane) - 1));
+                        __syncwarp();
+                        if (ok) {
+                            w.bd[pos] = d;
+                            w.bn[pos] = nn;
+                        }
+                        __syncwarp();
+                        pool_merge(topk, tsize, w.bd, w.bn, __popc(om), lane);
+                    }
+                    __syncwarp();
+                }
+                if (R > 0) {  // twin pool depends on the offer order
+                    for (uint32_t i = 0; i < nnew; ++i) {
+                        const uint32_t pos = w.nnew[i];
+                        const uint32_t node = w.nb[pos];
+                        if (!is_deleted(node)) topk_offer_seq(node, w.nd[pos], w.nd[pos]);
+                    }
+                }
+            } else {
+                // context propagation over the whole list (lane 0, reach order)
+                if (propagate && lane == 0) {
+                    const uint32_t hop = uhop + 1;
+                    for (uint32_t i = 0; i < nbc; ++i) {
+                        const uint32_t o = w.nb[i];
+                        bool changed = false;
+                        const uint64_t eb = c.ent_ptr[o], ee = c.ent_ptr[o + 1];
+                        for (uint64_t e = eb; e < ee; ++e) {
+                            const uint32_t ent = c.ent_idx[e];
+                            if (has_relation(a, uent, ent)) {
+                                changed |= assign_ctx(o, ent, hop);
+                                break;
+                            }
+                        }
+                        for (uint32_t j = 0; j < nlc; ++j)
+                            if (w.lc[2 * j] == o) changed |= assign_ctx(o, w.lc[2 * j + 1], hop);
+                        if (changed) w.nflag[i] |= 2;
+                    }
+                }
+                ctx_used = __shfl_sync(kFull, ctx_used, 0);
+                __syncwarp();
+                if (ctx_used * 2 > a.ctxcap) err |= ERR_CTX;
+                // raw distance of re-offered (context-changed) old nodes
+                for (uint32_t b = 0; b < nbc; b += 32) {
+                    const uint32_t i = b + lane;
+                    if (i < nbc && w.nflag[i] == 2) w.nd[i] = -hybrid_score(c, sq, w.nb[i]);
+                }
+                __syncwarp();
+                for (uint32_t i = 0; i < nbc; ++i) {
+                    if (!w.nflag[i]) continue;  // unchanged old node: a no-op offer
+                    const uint32_t o = w.nb[i];
+                    const double raw = w.nd[i];
+                    const double d = adjusted(raw, o);
+                    const uint32_t fl = (expbits && bit_test(expbits, o)) ? kFlagExp : 0u;
+                    pool_offer(cand, csize, d, o, fl, lane);
+                    if (!is_deleted(o)) topk_offer_seq(o, d, raw);
+                }
+                cursor = 0;
+            }
+        }
+
+        // ---- keyword_postfilter (search.cpp:100-139) ---------------------
+        // candidates: topk (+ twin pool when keywords are required)
+        const uint32_t ntw = R > 0 ? min(ntwin, a.twcap) : 0;
+        if (lane == 0)
+            for (uint32_t i = 0; i < ntw; ++i) twin_raw[i] = adjusted(twin_raw[i], twin_node[i]);
+        __syncwarp();
+        uint32_t out = 0;
+        const uint32_t total = tsize + ntw;
+        while (out < K) {
+            // best remaining (dist, node) over topk ∪ twin
+            double bd = __longlong_as_double(0x7FF0000000000000ll);
+            uint32_t bnode = kEmpty;
+            for (uint32_t i = lane; i < total; i += 32) {
+                const double d = i < tsize ? w.topk_d[i] : twin_raw[i - tsize];
+                const uint32_t nn = i < tsize ? w.topk_n[i] : twin_node[i - tsize];
+                if (nn != kEmpty && eless(d, nn, bd, bnode)) {
+                    bd = d;
+                    bnode = nn;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(kFull, bd, o);
+                const uint32_t on = __shfl_xor_sync(kFull, bnode, o);
+                if (eless(od, on, bd, bnode)) {
+                    bd = od;
+                    bnode = on;
+                }
+            }
+            if (bnode == kEmpty) break;
+            for (uint32_t i = lane; i < total; i += 32) {  // consume every copy of the node
+                if (i < tsize) {
+                    if (w.topk_n[i] == bnode) w.topk_n[i] = kEmpty;
+                } else if (twin_node[i - tsize] == bnode) {
+                    twin_node[i - tsize] = kEmpty;
+                }
+            }
+            __syncwarp();
+            if (is_deleted(bnode)) continue;
+            if (R > 0) {
+                bool all = true, any = false;
+                const uint64_t kb = c.kw_ptr[bnode], ke = c.kw_ptr[bnode + 1];
+                for (uint32_t i = lane; i < R; i += 32) {
+                    const bool h = sorted_contains(c.kw_idx, kb, ke, w.req[i]);
+                    all &= h;
+                    any |= h;
+                }
+                all = __all_sync(kFull, all);
+                any = __any_sync(kFull, any);
+                if (a.conjunctive ? !all : !any) continue;
+            }
+            if (lane == 0) {
+                a.r_node[(uint64_t)qi * a.hit_stride + out] = bnode;
+                a.r_score[(uint64_t)qi * a.hit_stride + out] = -bd;
+            }
+            ++out;
+        }
+        if (lane == 0) {
+            a.r_count[qi] = out;
+            a.r_expanded[qi] = expanded;
+            a.r_scored[qi] = scored;
+            uint32_t warn = (flags & QF_FALLBACK) ? 1u : 0u;
+            if (R > 0 && out < K) warn |= 2u;
+            a.r_warn[qi] = warn;
+            a.r_err[qi] = err;
+        }
+
+        // ---- reset per-warp scratch ---------------------------------------
+        if (ntouched > a.tcap) tover = true;
+        if (!tover) {
+            for (uint32_t i = lane; i < ntouched; i += 32) {
+                const uint32_t x = touched[i];
+                visited[x >> 5] = 0;
+                if (expbits) expbits[x >> 5] = 0;
+                if (twinbits) twinbits[x >> 5] = 0;
+            }
+        } else {
+            for (uint64_t i = lane; i < a.nwords; i += 32) {
+                visited[i] = 0;
+                if (expbits) expbits[i] = 0;
+                if (twinbits) twinbits[i] = 0;
+            }
+        }
+        if (ctx) {
+            for (uint32_t i = lane; i < a.ctxcap; i += 32) ctx[i] = make_uint4(kEmpty, 0, 0, 0);
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+}  // namespace fgb
+
+using namespace fgb;
+
+extern "C" {
+
+int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_opts* opts,
+                   fg_search_results* out) {
+    return guarded([&] {
+        if (!cix || !q || !out) throw Error("invalid-argument", "null pointer");
+        fg_index* ix = const_cast<fg_index*>(cix);
+        fg_corpus& c = *ix->corpus;
+        FGB_CUDA(cudaSetDevice(c.device));
+        cudaStream_t s = c.stream;
+        const uint64_t nq = q->count;
+        const uint32_t entry_count = opts ? opts->entry_count : 32;
+        const bool conj = opts ? opts->conjunctive_filter != 0 : true;
+        const uint64_t n = c.n;
+
+        // ---- host: validation (types.cpp:20-27) and seeds (search.cpp:67-98)
+        std::vector<uint8_t> qflags(nq, 0);
+        std::vector<std::string> errs(nq);
+        std::vector<uint64_t> seed_ptr(nq + 1, 0);
+        std::vector<uint32_t> seed_node, seed_ent;
+        std::vector<uint8_t> seed_has;
+        uint32_t max_k = 1, max_beam = 1, max_seeds = 0;
+        const uint32_t norm_seeds = static_cast<uint32_t>(std::min<uint64_t>(entry_count, n));
+        for (uint64_t i = 0; i < nq; ++i) {
+            const fg_weights wt = q->weights ? q->weights[i] : fg_weights{1.f, 1.f, 1.f, 0.f};
+            const uint32_t k = q->k ? q->k[i] : 10;
+            const uint32_t beam = q->beam_width ? q->beam_width[i] : 64;
+            const uint64_t ne = q->entities.ptr ? q->entities.ptr[i + 1] - q->entities.ptr[i] : 0;
+            try {
+                const float parts[4] = {wt.dense, wt.learned, wt.statistical, wt.entity};
+                for (float p : parts)
+                    if (!std::isfinite(p) || p < 0.0f)
+                        throw Error("invalid-weights", "weights must be finite and non-negative");
+                if (wt.dense <= 0.0f && wt.learned <= 0.0f && wt.statistical <= 0.0f)
+                    throw Error("invalid-weights", "at least one vector-path weight must be positive");
+                if (k == 0) throw Error("invalid-k", "k must be positive");
+                if (beam < k) throw Error("beam-too-small", "beam_width must be at least k");
+                if (wt.entity > 0.0f && ne == 0)
+                    throw Error("entities-required",
+                                "entity weight is positive but the query names no entities");
+                if (q->dense_dim != c.dim)
+                    throw Error("dim-mismatch", "dense dimensions differ: " +
+                                                    std::to_string(q->dense_dim) + " vs " +
+                                                    std::to_string(c.dim));
+            } catch (const Error& e) {
+                errs[i] = e.what();
+                seed_ptr[i + 1] = seed_node.size();
+                continue;
+            }
+            uint8_t f = QF_VALID;
+            if (ne > 0 && wt.entity > 0.0f) {
+                std::vector<std::pair<uint32_t, uint32_t>> seeds;  // (node, entity)
+                for (uint64_t j = q->entities.ptr[i]; j < q->entities.ptr[i + 1]; ++j) {
+                    const uint32_t e = q->entities.idx[j];
+                    auto it = ix->entity_map.find(e);
+                    if (it == ix->entity_map.end()) continue;
+                    for (uint32_t node : it->second) seeds.emplace_back(node, e);
+                }
+                if (!seeds.empty()) {
+                    std::sort(seeds.begin(), seeds.end());
+                    uint32_t cnt = 0;
+                    for (size_t j = 0; j < seeds.size(); ++j) {
+                        if (j > 0 && seeds[j].first == seeds[j - 1].first) continue;
+                        seed_node.push_back(seeds[j].first);
+                        seed_ent.push_back(seeds[j].second);
+                        seed_has.push_back(1);
+                        ++cnt;
+                    }
+                    max_seeds = std::max(max_seeds, cnt);
+                    f |= QF_ENTITY;
+                } else {
+                    f |= QF_FALLBACK;
+                }
+            }
+            seed_ptr[i + 1] = seed_node.size();
+            qflags[i] = f;
+            max_k = std::max(max_k, k);
+            max_beam = std::max(max_beam, beam);
+        }
+        if (out->hit_stride < max_k && nq) throw Error("invalid-argument", "hit_stride < max k");
+        bool any_ctx = false, any_req = false;
+        uint32_t max_req = 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            any_ctx |= (qflags[i] & QF_ENTITY) != 0;
+            const uint64_t r = q->required_keywords.ptr
+                                   ? q->required_keywords.ptr[i + 1] - q->required_keywords.ptr[i]
+                                   : 0;
+            if ((qflags[i] & QF_VALID) && r) {
+                any_req = true;
+                max_req = std::max<uint32_t>(max_req, static_cast<uint32_t>(r));
+            }
+        }
+
+        // ---- device copies of the batch
+        QueryUpload up;
+        up.upload(*q, s);
+        DevBuf<uint64_t> d_sptr;
+        DevBuf<uint32_t> d_snode, d_sent;
+        DevBuf<uint8_t> d_shas, d_qflags;
+        d_sptr.upload(seed_ptr, s);
+        if (seed_node.empty()) {
+            seed_node.push_back(0);
+            seed_ent.push_back(0);
+            seed_has.push_back(0);
+        }
+        d_snode.upload(seed_node, s);
+        d_sent.upload(seed_ent, s);
+        d_shas.upload(seed_has, s);
+        d_qflags.upload(qflags.empty() ? std::vector<uint8_t>(1, 0) : qflags, s);
+        const uint32_t stride = std::max(out->hit_stride, 1u);
+        DevBuf<uint32_t> r_node(std::max<uint64_t>(nq * stride, 1)), r_count(std::max<uint64_t>(nq, 1)),
+            r_warn(std::max<uint64_t>(nq, 1)), r_err(std::max<uint64_t>(nq, 1));
+        DevBuf<double> r_score(std::max<uint64_t>(nq * stride, 1));
+        DevBuf<unsigned long long> r_exp(std::max<uint64_t>(nq, 1)), r_sc(std::max<uint64_t>(nq, 1));
+        DevBuf<unsigned int> work(1);
+        work.zero(s);
+
+        // ---- geometry
+        SearchArgs a{};
+        a.c = c.dc;
+        a.semantic = ix->semantic.get();
+        a.degree = ix->degree;
+        a.kw_ptr = ix->kw_ptr.get();
+        a.kw_idx = ix->kw_idx.get();
+        a.lg_ptr = ix->lg_ptr.get();
+        a.lg = ix->lg.get();
+        a.kg_ptr = ix->kg_ptr.get();
+        a.kg_nbr = ix->kg_nbr.get();
+        a.kg_rows = ix->kg_rows;
+        a.q = up.dq;
+        a.seed_ptr = d_sptr.get();
+        a.seed_node = d_snode.get();
+        a.seed_ent = d_sent.get();
+        a.seed_has = d_shas.get();
+        a.norm_order = ix->norm_order.get();
+        a.entry_count = norm_seeds;
+        a.qflags = d_qflags.get();
+        a.conjunctive = conj ? 1 : 0;
+        a.lcap = hash_capacity(up.max_lnnz);
+        a.scap = hash_capacity(up.max_snnz);
+        a.beamcap = std::max(max_beam, 32u);
+        a.kcap = std::max(max_k, 1u);
+        a.lccap = std::max(ix->max_logical_group, 1u);
+        a.nbcap = ix->degree + (any_req ? ix->max_kw_edges : 0) + (any_ctx ? a.lccap : 0) + 32;
+        a.reqcap = std::max(max_req, 1u);
+        auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
+        size_t ws = al(static_cast<size_t>(c.dstride) * 4 + static_cast<size_t>(a.lcap + a.scap) * 8);
+        ws += al(a.beamcap * 8) + 2 * al(a.kcap * 8) + al(a.nbcap * 8) + al(32 * 8);
+        ws += al(a.beamcap * 4) + al(a.kcap * 4) + 2 * al(a.nbcap * 4) + al(a.nbcap);
+        ws += al(a.lccap * 8 + 8) + al(a.reqcap * 4 + 4) + al(32 * 4);
+        a.warp_smem = static_cast<uint32_t>(ws);
+        const size_t block_smem = ws * kWarpsPerBlock;
+        if (block_smem > 227 * 1024)
+            throw Error("beam-too-small", "beam/query too large for the search kernel's shared memory");
+        FGB_CUDA(cudaFuncSetAttribute(search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)block_smem));
+        int per_sm = 0, sms = 0;
+        FGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, search_kernel,
+                                                               kWarpsPerBlock * 32, block_smem));
+        FGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+        per_sm = std::max(per_sm, 1);
+        const uint64_t want_blocks = (nq + kWarpsPerBlock - 1) / kWarpsPerBlock;
+        const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(want_blocks, (uint64_t)sms * per_sm));
+        const uint64_t slots = blocks * kWarpsPerBlock;
+
+        // ---- per-warp scratch (reused across calls)
+        a.nwords = (n + 31) / 32;
+        a.tcap = 16384;
+        a.twcap = any_req ? 8192 : 0;
+        a.ctxcap = any_ctx ? 8192 : 0;
+        const uint64_t nbitsets = 1 + (any_ctx ? 1 : 0) + (any_req ? 1 : 0);
+        const uint64_t bits_words = slots * a.nwords * nbitsets;
+        if (ix->scratch_bits.size() < bits_words) {
+            ix->scratch_bits.alloc(bits_words);
+            ix->scratch_bits.zero(s);
+        }
+        uint32_t* bits = ix->scratch_bits.get();
+        a.visited = bits;
+        a.expbits = any_ctx ? bits + slots * a.nwords : nullptr;
+        a.twinbits = any_req ? bits + slots * a.nwords * (any_ctx ? 2 : 1) : nullptr;
+        const uint64_t list_words = slots * (a.tcap + a.twcap);
+        ix->scratch_lists.ensure(std::max<uint64_t>(list_words, 1));
+        a.touched = ix->scratch_lists.get();
+        a.twin_node = any_req ? a.touched + slots * a.tcap : nullptr;
+        const uint64_t misc = slots * (static_cast<uint64_t>(a.twcap) * 8 + static_cast<uint64_t>(a.ctxcap) * 16);
+        ix->scratch_misc.ensure(std::max<uint64_t>(misc, 16));
+        a.twin_raw = any_req ? reinterpret_cast<double*>(ix->scratch_misc.get()) : nullptr;
+        a.ctx = any_ctx ? reinterpret_cast<uint4*>(ix->scratch_misc.get() + slots * a.twcap * 8) : nullptr;
+        if (any_ctx) FGB_CUDA(cudaMemsetAsync(a.ctx, 0xFF, slots * a.ctxcap * 16, s));
+        a.hit_stride = stride;
+        a.r_node = r_node.get();
+        a.r_score = r_score.get();
+        a.r_count = r_count.get();
+        a.r_expanded = r_exp.get();
+        a.r_scored = r_sc.get();
+        a.r_warn = r_warn.get();
+        a.r_err = r_err.get();
+        a.work = work.get();
+
+        FGB_CUDA(cudaEventRecord(ix->ev0, s));
+        if (nq) search_kernel<<<(unsigned)blocks, kWarpsPerBlock * 32, block_smem, s>>>(a);
+        FGB_LAUNCH("search_kernel");
+        FGB_CUDA(cudaEventRecord(ix->ev1, s));
+
+        std::vector<uint32_t> h_node(nq * stride), h_count(nq), h_warn(nq), h_err(nq);
+        std::vector<double> h_score(nq * stride);
+        std::vector<unsigned long long> h_exp(nq), h_sc(nq);
+        r_node.download(h_node.data(), nq * stride, s);
+        r_score.download(h_score.data(), nq * stride, s);
+        r_count.download(h_count.data(), nq, s);
+        r_warn.download(h_warn.data(), nq, s);
+        r_err.download(h_err.data(), nq, s);
+        r_exp.download(h_exp.data(), nq, s);
+        r_sc.download(h_sc.data(), nq, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        float ms = 0;
+        FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
+        ix->last_kernel_ms = ms;
+        ix->last_launches = nq ? 1 : 0;
+        for (uint64_t i = 0; i < nq; ++i) {
+            if (h_err[i])
+                throw Error("internal", "search scratch overflow (twin/context table) on query " +
+                                            std::to_string(i));
+            const uint32_t cnt = errs[i].empty() ? h_count[i] : 0;
+            out->hit_count[i] = cnt;
+            for (uint32_t j = 0; j < cnt; ++j) {
+                const uint32_t node = h_node[i * stride + j];
+                out->node[i * out->hit_stride + j] = node;
+                out->doc_id[i * out->hit_stride + j] = c.doc_id[node];
+                out->score[i * out->hit_stride + j] = h_score[i * stride + j];
+            }
+            if (out->expanded) out->expanded[i] = errs[i].empty() ? h_exp[i] : 0;
+            if (out->scored) out->scored[i] = errs[i].empty() ? h_sc[i] : 0;
+            if (out->warnings) out->warnings[i] = errs[i].empty() ? h_warn[i] : 0;
+            if (out->errors && out->error_stride) {
+                char* dst = out->errors + i * out->error_stride;
+                std::strncpy(dst, errs[i].c_str(), out->error_stride - 1);
+                dst[out->error_stride - 1] = 0;
+            }
+        }
+    });
+}
+
+int fg_last_search_stats(const fg_index* ix, double* kernel_ms, uint64_t* launches) {
+    return guarded([&] {
+        if (kernel_ms) *kernel_ms = ix->last_kernel_ms;
+        if (launches) *launches = ix->last_launches;
+    });
+}
+
+}  // extern "C"
