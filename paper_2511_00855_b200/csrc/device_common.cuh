@@ -102,31 +102,32 @@ struct SmemQuery {
 
 // Dense dot of the staged query against row `node`, sequential over i.
 __device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q, uint64_t node) {
+    // Software-pipelined: the next kStage float4 of the row are in flight
+    // while the current ones feed the (inherently sequential) fp64 chain.
+    constexpr uint32_t kStage = 8;
     const float4* row = reinterpret_cast<const float4*>(c.dense + node * c.dstride);
     const float4* q4 = reinterpret_cast<const float4*>(q);
     const uint32_t n4 = c.dstride >> 2;
     double acc = 0.0;
-    uint32_t i = 0;
-    for (; i + 4 <= n4; i += 4) {
-        float4 d[4];
+    float4 cur[kStage], nxt[kStage];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) d[j] = __ldg(row + i + j);
+    for (uint32_t j = 0; j < kStage; ++j) cur[j] = j < n4 ? __ldg(row + j) : make_float4(0, 0, 0, 0);
+    for (uint32_t i = 0; i < n4; i += kStage) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float4 qq = q4[i + j];
-            acc = __fma_rn((double)qq.x, (double)d[j].x, acc);
-            acc = __fma_rn((double)qq.y, (double)d[j].y, acc);
-            acc = __fma_rn((double)qq.z, (double)d[j].z, acc);
-            acc = __fma_rn((double)qq.w, (double)d[j].w, acc);
+        for (uint32_t j = 0; j < kStage; ++j)
+            nxt[j] = i + kStage + j < n4 ? __ldg(row + i + kStage + j) : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (uint32_t j = 0; j < kStage; ++j) {
+            if (i + j < n4) {
+                const float4 qq = q4[i + j];
+                acc = __fma_rn((double)qq.x, (double)cur[j].x, acc);
+                acc = __fma_rn((double)qq.y, (double)cur[j].y, acc);
+                acc = __fma_rn((double)qq.z, (double)cur[j].z, acc);
+                acc = __fma_rn((double)qq.w, (double)cur[j].w, acc);
+            }
         }
-    }
-    for (; i < n4; ++i) {
-        const float4 d = __ldg(row + i);
-        const float4 qq = q4[i];
-        acc = __fma_rn((double)qq.x, (double)d.x, acc);
-        acc = __fma_rn((double)qq.y, (double)d.y, acc);
-        acc = __fma_rn((double)qq.z, (double)d.z, acc);
-        acc = __fma_rn((double)qq.w, (double)d.w, acc);
+#pragma unroll
+        for (uint32_t j = 0; j < kStage; ++j) cur[j] = nxt[j];
     }
     return acc;
 }
@@ -137,18 +138,41 @@ __device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q
 __device__ __forceinline__ double sparse_chain(const uint32_t* idx, const float* val, uint64_t off,
                                                uint32_t nnz, const uint32_t* keys,
                                                const float* vals, uint32_t mask) {
+    constexpr uint32_t kStage = 4;  // 16 entries per stage, next stage in flight
     double acc = 0.0;
     const uint4* i4 = reinterpret_cast<const uint4*>(idx + off);
     const float4* v4 = reinterpret_cast<const float4*>(val + off);
     const uint32_t n4 = (nnz + 3) >> 2;
-    for (uint32_t i = 0; i < n4; ++i) {
-        const uint4 ii = __ldg(i4 + i);
-        const float4 vv = __ldg(v4 + i);
-        float q;
-        if (ii.x != kPad && hash_find(keys, vals, mask, ii.x, q)) acc = __fma_rn((double)q, (double)vv.x, acc);
-        if (ii.y != kPad && hash_find(keys, vals, mask, ii.y, q)) acc = __fma_rn((double)q, (double)vv.y, acc);
-        if (ii.z != kPad && hash_find(keys, vals, mask, ii.z, q)) acc = __fma_rn((double)q, (double)vv.z, acc);
-        if (ii.w != kPad && hash_find(keys, vals, mask, ii.w, q)) acc = __fma_rn((double)q, (double)vv.w, acc);
+    const uint4 padi = make_uint4(kPad, kPad, kPad, kPad);
+    uint4 ci[kStage], ni[kStage];
+    float4 cv[kStage], nv[kStage];
+#pragma unroll
+    for (uint32_t j = 0; j < kStage; ++j) {
+        ci[j] = j < n4 ? __ldg(i4 + j) : padi;
+        cv[j] = j < n4 ? __ldg(v4 + j) : make_float4(0, 0, 0, 0);
+    }
+    for (uint32_t i = 0; i < n4; i += kStage) {
+#pragma unroll
+        for (uint32_t j = 0; j < kStage; ++j) {
+            const bool in = i + kStage + j < n4;
+            ni[j] = in ? __ldg(i4 + i + kStage + j) : padi;
+            nv[j] = in ? __ldg(v4 + i + kStage + j) : make_float4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < kStage; ++j) {
+            const uint4 ii = ci[j];
+            const float4 vv = cv[j];
+            float q;
+            if (ii.x != kPad && hash_find(keys, vals, mask, ii.x, q)) acc = __fma_rn((double)q, (double)vv.x, acc);
+            if (ii.y != kPad && hash_find(keys, vals, mask, ii.y, q)) acc = __fma_rn((double)q, (double)vv.y, acc);
+            if (ii.z != kPad && hash_find(keys, vals, mask, ii.z, q)) acc = __fma_rn((double)q, (double)vv.z, acc);
+            if (ii.w != kPad && hash_find(keys, vals, mask, ii.w, q)) acc = __fma_rn((double)q, (double)vv.w, acc);
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < kStage; ++j) {
+            ci[j] = ni[j];
+            cv[j] = nv[j];
+        }
     }
     return acc;
 }

@@ -286,7 +286,7 @@ size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uin
 uint32_t pool_capacity(uint64_t n, uint32_t k) {
     const uint64_t worst = std::min<uint64_t>(n, 4ull * k * k + k);
     uint32_t cap = kPassThreads;
-    while (cap < 2 * worst) cap <<= 1;
+    while (cap < worst + worst / 2) cap <<= 1;  // load factor <= 2/3 at the worst case
     return cap;
 }
 
