@@ -101,10 +101,10 @@ struct SmemQuery {
 };
 
 // Dense dot of the staged query against row `node`, sequential over i.
+template <uint32_t kStage = 8>
 __device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q, uint64_t node) {
     // Software-pipelined: the next kStage float4 of the row are in flight
     // while the current ones feed the (inherently sequential) fp64 chain.
-    constexpr uint32_t kStage = 8;
     const float4* row = reinterpret_cast<const float4*>(c.dense + node * c.dstride);
     const float4* q4 = reinterpret_cast<const float4*>(q);
     const uint32_t n4 = c.dstride >> 2;
@@ -179,9 +179,10 @@ __device__ __forceinline__ double sparse_chain(const uint32_t* idx, const float*
 
 // hybrid_score(weighted query, doc) (scoring.cpp:88-99): dense, then learned,
 // then statistical, in that fixed order.
+template <uint32_t kStage = 8>
 __device__ __forceinline__ double hybrid_score(const DevCorpus& c, const SmemQuery& q,
                                                uint64_t node) {
-    double acc = q.dense ? dense_chain(c, q.dense, node) : 0.0;
+    double acc = q.dense ? dense_chain<kStage>(c, q.dense, node) : 0.0;
     if (q.lmask) {
         const double l = sparse_chain(c.l_idx, c.l_val, c.l_off[node], c.l_nnz[node], q.lkeys,
                                       q.lvals, q.lmask);

@@ -37,7 +37,7 @@ namespace {
 
 constexpr uint32_t kFlagExp = 0x80000000u;  // cand entry expanded
 constexpr uint32_t kNodeMask = 0x7FFFFFFFu;
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 1;  // one query-warp per CTA: CTAs pack SMs by smem
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 enum : uint32_t { QF_VALID = 1, QF_ENTITY = 2, QF_FALLBACK = 4 };
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                     has = a.seed_has[sb + i] != 0;
                 }
                 bit_test_set(visited, node);
-                raw = -hybrid_score(c, sq, node);
+                raw = -hybrid_score<12>(c, sq, node);
             }
             touch(node, v);
             scored += __popc(__ballot_sync(kFull, v));
@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                 const uint32_t i = b + lane;
                 if (i < nnew) {
                     const uint32_t pos = w.nnew[i];
-                    w.nd[pos] = -hybrid_score(c, sq, w.nb[pos]);
+                    w.nd[pos] = -hybrid_score<12>(c, sq, w.nb[pos]);
                 }
             }
             __syncwarp();
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                 // raw distance of re-offered (context-changed) old nodes
                 for (uint32_t b = 0; b < nbc; b += 32) {
                     const uint32_t i = b + lane;
-                    if (i < nbc && w.nflag[i] == 2) w.nd[i] = -hybrid_score(c, sq, w.nb[i]);
+                    if (i < nbc && w.nflag[i] == 2) w.nd[i] = -hybrid_score<12>(c, sq, w.nb[i]);
                 }
                 __syncwarp();
                 for (uint32_t i = 0; i < nbc; ++i) {
