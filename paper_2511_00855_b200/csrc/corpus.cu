@@ -173,10 +173,6 @@ void QueryUpload::upload(const fg_query_view& q, cudaStream_t s) {
                     req_ptr.get(), req_idx.get(), k.get(),    beam.get(),    hops.get()};
 }
 
-// Bytes of shared memory stage_query needs for hash capacities lcap/scap.
-size_t stage_bytes(uint32_t dstride, uint32_t lcap, uint32_t scap) {
-    return static_cast<size_t>(dstride) * 4 + static_cast<size_t>(lcap + scap) * 8;
-}
 
 }  // namespace fgb
 

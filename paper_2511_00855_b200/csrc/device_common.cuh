@@ -26,7 +26,7 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // empty hash slot
 //  dense   n x dstride fp32, dstride = dim rounded up to 4 (16-B rows, zero pad)
 //  sparse  per path: row offset (multiple of 4 entries) + nnz, idx/val arrays
 //          padded per row to a multiple of 4 with (kPad, 0) so rows load as
-//          uint4/float4
+//          uint4/float4 (and bulk-copy at 16-B granularity)
 //  keywords, entities: plain CSR (sorted ids per doc)
 struct DevCorpus {
     uint64_t n;
@@ -88,25 +88,69 @@ __host__ __device__ inline uint32_t hash_capacity(uint32_t nnz) {
     return c;
 }
 
+// Bit filter in front of each hash: 2 * capacity words = 64 filter bits per
+// hash slot (>= 128 per query term), so a document term that is not a query
+// term is rejected by one shared-memory load and a bit test; only filter hits
+// (the ~nnz-overlap true matches plus <1% false positives) probe the hash.
+__host__ __device__ inline uint32_t filter_words(uint32_t cap) { return 2 * cap; }
+
+__device__ __forceinline__ bool filter_hit(const uint32_t* f, uint32_t fmask, uint32_t key) {
+    return (f[(key >> 5) & fmask] >> (key & 31)) & 1u;
+}
+
 // A weighted query (or a document acting as one) staged in shared memory:
-// dense part (dstride floats, zero padded) and one hash per sparse path.
+// dense part as fp64 (dstride doubles, zero padded — the exact widening of
+// the fp32 weighted values, so the chain needs one conversion per product),
+// and per sparse path a bit filter + hash.
 struct SmemQuery {
-    const float* dense;  // nullptr: dense path disabled (weight 0) -> contributes +0.0
+    const double* dense;  // nullptr: dense path disabled (weight 0) -> contributes +0.0
     const uint32_t* lkeys;
     const float* lvals;
-    uint32_t lmask;      // 0: learned path empty/disabled
+    const uint32_t* lfilt;
+    uint32_t lmask;       // 0: learned path empty/disabled
     const uint32_t* skeys;
     const float* svals;
+    const uint32_t* sfilt;
     uint32_t smask;
 };
 
+// Bytes a staged query/document occupies in shared memory.
+__host__ __device__ inline size_t stage_bytes(uint32_t dstride, uint32_t lcap, uint32_t scap) {
+    return static_cast<size_t>(dstride) * 8 +
+           static_cast<size_t>(lcap + scap) * 8 +
+           static_cast<size_t>(filter_words(lcap) + filter_words(scap)) * 4;
+}
+
+struct StagePtrs {
+    double* dense;
+    uint32_t* lkeys;
+    float* lvals;
+    uint32_t* lfilt;
+    uint32_t* skeys;
+    float* svals;
+    uint32_t* sfilt;
+};
+
+__device__ __forceinline__ StagePtrs stage_layout(unsigned char* smem, uint32_t dstride,
+                                                  uint32_t lcap, uint32_t scap) {
+    StagePtrs p;
+    p.dense = reinterpret_cast<double*>(smem);
+    p.lkeys = reinterpret_cast<uint32_t*>(p.dense + dstride);
+    p.lvals = reinterpret_cast<float*>(p.lkeys + lcap);
+    p.skeys = reinterpret_cast<uint32_t*>(p.lvals + lcap);
+    p.svals = reinterpret_cast<float*>(p.skeys + scap);
+    p.lfilt = reinterpret_cast<uint32_t*>(p.svals + scap);
+    p.sfilt = p.lfilt + filter_words(lcap);
+    return p;
+}
+
 // Dense dot of the staged query against row `node`, sequential over i.
 template <uint32_t kStage = 8>
-__device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q, uint64_t node) {
+__device__ __forceinline__ double dense_chain(const DevCorpus& c, const double* q, uint64_t node) {
     // Software-pipelined: the next kStage float4 of the row are in flight
     // while the current ones feed the (inherently sequential) fp64 chain.
     const float4* row = reinterpret_cast<const float4*>(c.dense + node * c.dstride);
-    const float4* q4 = reinterpret_cast<const float4*>(q);
+    const double2* q2 = reinterpret_cast<const double2*>(q);
     const uint32_t n4 = c.dstride >> 2;
     double acc = 0.0;
     float4 cur[kStage], nxt[kStage];
@@ -119,11 +163,11 @@ __device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q
 #pragma unroll
         for (uint32_t j = 0; j < kStage; ++j) {
             if (i + j < n4) {
-                const float4 qq = q4[i + j];
-                acc = __fma_rn((double)qq.x, (double)cur[j].x, acc);
-                acc = __fma_rn((double)qq.y, (double)cur[j].y, acc);
-                acc = __fma_rn((double)qq.z, (double)cur[j].z, acc);
-                acc = __fma_rn((double)qq.w, (double)cur[j].w, acc);
+                const double2 a = q2[2 * (i + j)], b = q2[2 * (i + j) + 1];
+                acc = __fma_rn(a.x, (double)cur[j].x, acc);
+                acc = __fma_rn(a.y, (double)cur[j].y, acc);
+                acc = __fma_rn(b.x, (double)cur[j].z, acc);
+                acc = __fma_rn(b.y, (double)cur[j].w, acc);
             }
         }
 #pragma unroll
@@ -132,12 +176,23 @@ __device__ __forceinline__ double dense_chain(const DevCorpus& c, const float* q
     return acc;
 }
 
+// One probe of a (filtered) query path: adds q_t * v in the chain when t is a
+// query term.  Terms arrive in ascending order (sorted rows).
+__device__ __forceinline__ void probe_term(uint32_t t, float v, const uint32_t* keys,
+                                           const float* vals, uint32_t mask,
+                                           const uint32_t* filt, double& acc) {
+    if (t == kPad || !filter_hit(filt, 2 * mask + 1, t)) return;
+    float q;
+    if (hash_find(keys, vals, mask, t, q)) acc = __fma_rn((double)q, (double)v, acc);
+}
+
 // Sparse dot: walk the document row in ascending index order and probe the
-// query's hash; matches accumulate in ascending shared-index order, exactly
-// the merge/probe order of sparse_dot_impl (scoring.cpp:24-74).
+// query's filter+hash; matches accumulate in ascending shared-index order,
+// exactly the merge/probe order of sparse_dot_impl (scoring.cpp:24-74).
 __device__ __forceinline__ double sparse_chain(const uint32_t* idx, const float* val, uint64_t off,
                                                uint32_t nnz, const uint32_t* keys,
-                                               const float* vals, uint32_t mask) {
+                                               const float* vals, uint32_t mask,
+                                               const uint32_t* filt) {
     constexpr uint32_t kStage = 4;  // 16 entries per stage, next stage in flight
     double acc = 0.0;
     const uint4* i4 = reinterpret_cast<const uint4*>(idx + off);
@@ -160,13 +215,10 @@ __device__ __forceinline__ double sparse_chain(const uint32_t* idx, const float*
         }
 #pragma unroll
         for (uint32_t j = 0; j < kStage; ++j) {
-            const uint4 ii = ci[j];
-            const float4 vv = cv[j];
-            float q;
-            if (ii.x != kPad && hash_find(keys, vals, mask, ii.x, q)) acc = __fma_rn((double)q, (double)vv.x, acc);
-            if (ii.y != kPad && hash_find(keys, vals, mask, ii.y, q)) acc = __fma_rn((double)q, (double)vv.y, acc);
-            if (ii.z != kPad && hash_find(keys, vals, mask, ii.z, q)) acc = __fma_rn((double)q, (double)vv.z, acc);
-            if (ii.w != kPad && hash_find(keys, vals, mask, ii.w, q)) acc = __fma_rn((double)q, (double)vv.w, acc);
+            probe_term(ci[j].x, cv[j].x, keys, vals, mask, filt, acc);
+            probe_term(ci[j].y, cv[j].y, keys, vals, mask, filt, acc);
+            probe_term(ci[j].z, cv[j].z, keys, vals, mask, filt, acc);
+            probe_term(ci[j].w, cv[j].w, keys, vals, mask, filt, acc);
         }
 #pragma unroll
         for (uint32_t j = 0; j < kStage; ++j) {
@@ -183,20 +235,12 @@ template <uint32_t kStage = 8>
 __device__ __forceinline__ double hybrid_score(const DevCorpus& c, const SmemQuery& q,
                                                uint64_t node) {
     double acc = q.dense ? dense_chain<kStage>(c, q.dense, node) : 0.0;
-    if (q.lmask) {
-        const double l = sparse_chain(c.l_idx, c.l_val, c.l_off[node], c.l_nnz[node], q.lkeys,
-                                      q.lvals, q.lmask);
-        acc = __dadd_rn(acc, l);
-    } else {
-        acc = __dadd_rn(acc, 0.0);
-    }
-    if (q.smask) {
-        const double s = sparse_chain(c.s_idx, c.s_val, c.s_off[node], c.s_nnz[node], q.skeys,
-                                      q.svals, q.smask);
-        acc = __dadd_rn(acc, s);
-    } else {
-        acc = __dadd_rn(acc, 0.0);
-    }
+    acc = __dadd_rn(acc, q.lmask ? sparse_chain(c.l_idx, c.l_val, c.l_off[node], c.l_nnz[node],
+                                                q.lkeys, q.lvals, q.lmask, q.lfilt)
+                                 : 0.0);
+    acc = __dadd_rn(acc, q.smask ? sparse_chain(c.s_idx, c.s_val, c.s_off[node], c.s_nnz[node],
+                                                q.skeys, q.svals, q.smask, q.sfilt)
+                                 : 0.0);
     return acc;
 }
 

@@ -25,12 +25,14 @@
 //    single-entry offers (exactly Pool::offer, search.cpp:26-42).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "fg_cuda.hpp"
 #include "index.hpp"
 #include "query_stage.cuh"
+#include "tma.cuh"
 
 namespace fgb {
 namespace {
@@ -65,6 +67,9 @@ struct SearchArgs {
     int conjunctive;
     uint32_t lcap, scap, beamcap, kcap, nbcap, lccap, reqcap;
     uint32_t warp_smem;
+    // TMA row staging: rb slots of slot_words 4-byte words each; inside a
+    // slot: dense [0, dstride), learned idx/val, statistical idx/val
+    uint32_t rb, slot_words, o_lidx, o_lval, o_sidx, o_sval;
     uint32_t* visited;
     uint32_t* expbits;
     uint32_t* twinbits;
@@ -107,6 +112,8 @@ struct WarpMem {
     uint32_t* req;    // required keywords (sorted)
     double* bd;       // batch sort buffer
     uint32_t* bn;
+    float* rows;      // rb staged document rows (TMA destination)
+    uint64_t* bar;    // mbarrier of the staging rounds
 };
 
 __device__ WarpMem carve(unsigned char* base, const SearchArgs& a) {
@@ -117,7 +124,7 @@ __device__ WarpMem carve(unsigned char* base, const SearchArgs& a) {
         off += (bytes + 15) & ~size_t(15);
         return p;
     };
-    m.stage = take(static_cast<size_t>(a.c.dstride) * 4 + static_cast<size_t>(a.lcap + a.scap) * 8);
+    m.stage = take(stage_bytes(a.c.dstride, a.lcap, a.scap));
     m.cand_d = reinterpret_cast<double*>(take(a.beamcap * 8));
     m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
     m.topk_raw = reinterpret_cast<double*>(take(a.kcap * 8));
@@ -131,7 +138,108 @@ __device__ WarpMem carve(unsigned char* base, const SearchArgs& a) {
     m.lc = reinterpret_cast<uint32_t*>(take(a.lccap * 8 + 8));
     m.req = reinterpret_cast<uint32_t*>(take(a.reqcap * 4 + 4));
     m.bn = reinterpret_cast<uint32_t*>(take(32 * 4));
+    m.bar = reinterpret_cast<uint64_t*>(take(16));
+    m.rows = reinterpret_cast<float*>(take(static_cast<size_t>(a.rb) * a.slot_words * 4));
     return m;
+}
+
+// ---------------------------------------------------------------- staged K1
+// Scores `count` nodes (node_of(i), i < count) against the staged query,
+// rb rows per round: every lane owning a row issues TMA bulk copies of its
+// dense row and sparse postings into its smem slot, one mbarrier completes
+// the round, then each lane runs its bit-exact chain from shared memory
+// (slot stride = 4 mod 32 words, so the lanes' 16-byte reads never conflict).
+template <typename NodeOf, typename Sink>
+__device__ void score_staged(const SearchArgs& a, const SmemQuery& sq, const WarpMem& w,
+                             uint32_t lane, uint32_t& phase, uint32_t count, NodeOf node_of,
+                             Sink sink) {
+    const DevCorpus& c = a.c;
+    if (a.rb == 0) {  // register path: each lane streams its own row
+        for (uint32_t b = 0; b < count; b += 32) {
+            if (b + lane < count) sink(b + lane, -hybrid_score<12>(c, sq, node_of(b + lane)));
+        }
+        __syncwarp();
+        return;
+    }
+    for (uint32_t b = 0; b < count; b += a.rb) {
+        const uint32_t cnt = min(a.rb, count - b);
+        const bool mine = lane < cnt;
+        uint32_t node = 0, ln = 0, sn = 0, bytes = 0;
+        uint64_t lo = 0, so = 0;
+        if (mine) {
+            node = node_of(b + lane);
+            if (sq.lmask) {
+                ln = c.l_nnz[node];
+                lo = c.l_off[node];
+            }
+            if (sq.smask) {
+                sn = c.s_nnz[node];
+                so = c.s_off[node];
+            }
+            bytes = (sq.dense ? c.dstride * 4 : 0) + ((ln + 3) & ~3u) * 8 + ((sn + 3) & ~3u) * 8;
+        }
+        uint32_t total = bytes;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(kFull, total, o);
+        if (lane == 0) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(w.bar, total);
+        }
+        __syncwarp();
+        float* slot = w.rows + static_cast<size_t>(lane) * a.slot_words;
+        if (mine) {
+            if (sq.dense) bulk_g2s(slot, c.dense + static_cast<uint64_t>(node) * c.dstride, c.dstride * 4, w.bar);
+            if (ln) {
+                const uint32_t nb = ((ln + 3) & ~3u) * 4;
+                bulk_g2s(slot + a.o_lidx, c.l_idx + lo, nb, w.bar);
+                bulk_g2s(slot + a.o_lval, c.l_val + lo, nb, w.bar);
+            }
+            if (sn) {
+                const uint32_t nb = ((sn + 3) & ~3u) * 4;
+                bulk_g2s(slot + a.o_sidx, c.s_idx + so, nb, w.bar);
+                bulk_g2s(slot + a.o_sval, c.s_val + so, nb, w.bar);
+            }
+        }
+        mbar_wait(w.bar, phase);
+        phase ^= 1u;
+        if (mine) {
+            double acc = 0.0;
+            if (sq.dense) {
+                const float4* r4 = reinterpret_cast<const float4*>(slot);
+                const double2* q2 = reinterpret_cast<const double2*>(sq.dense);
+                const uint32_t n4 = c.dstride >> 2;
+#pragma unroll 4
+                for (uint32_t i = 0; i < n4; ++i) {
+                    const float4 d = r4[i];
+                    const double2 qa = q2[2 * i], qb = q2[2 * i + 1];
+                    acc = __fma_rn(qa.x, (double)d.x, acc);
+                    acc = __fma_rn(qa.y, (double)d.y, acc);
+                    acc = __fma_rn(qb.x, (double)d.z, acc);
+                    acc = __fma_rn(qb.y, (double)d.w, acc);
+                }
+            }
+            auto sparse = [&](const uint32_t* idx, const float* val, uint32_t nnz, const uint32_t* keys,
+                              const float* vals, uint32_t mask, const uint32_t* filt) {
+                double s = 0.0;  // ascending index order, 16-byte smem reads
+                const uint4* i4 = reinterpret_cast<const uint4*>(idx);
+                const float4* v4 = reinterpret_cast<const float4*>(val);
+                for (uint32_t j = 0; j < (nnz + 3) / 4; ++j) {
+                    const uint4 ii = i4[j];
+                    const float4 vv = v4[j];
+                    probe_term(ii.x, vv.x, keys, vals, mask, filt, s);
+                    probe_term(ii.y, vv.y, keys, vals, mask, filt, s);
+                    probe_term(ii.z, vv.z, keys, vals, mask, filt, s);
+                    probe_term(ii.w, vv.w, keys, vals, mask, filt, s);
+                }
+                return s;
+            };
+            const uint32_t* si = reinterpret_cast<const uint32_t*>(slot);
+            acc = __dadd_rn(acc, ln ? sparse(si + a.o_lidx, slot + a.o_lval, ln, sq.lkeys, sq.lvals, sq.lmask, sq.lfilt) : 0.0);
+            acc = __dadd_rn(acc, sn ? sparse(si + a.o_sidx, slot + a.o_sval, sn, sq.skeys, sq.svals, sq.smask, sq.sfilt) : 0.0);
+            sink(b + lane, -acc);
+        }
+        __syncwarp();
+    }
 }
 
 // ---------------------------------------------------------------- pools
@@ -361,6 +469,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
     double* twin_raw = a.twin_raw ? a.twin_raw + slot * a.twcap : nullptr;
     uint4* ctx = a.ctx ? a.ctx + slot * a.ctxcap : nullptr;
     const DevCorpus& c = a.c;
+    uint32_t phase = 0;  // staging mbarrier phase (persists across queries)
+    if (lane == 0) {
+        mbar_init(w.bar, 1);
+        fence_proxy_async();
+    }
+    __syncwarp();
 
     while (true) {
         uint32_t qi = 0;
@@ -502,8 +616,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                     has = a.seed_has[sb + i] != 0;
                 }
                 bit_test_set(visited, node);
-                raw = -hybrid_score<12>(c, sq, node);
             }
+            const uint32_t cnt_s = min(32u, nseeds - base);
+            score_staged(a, sq, w, lane, phase, cnt_s,
+                         [&](uint32_t j) {
+                             return norm_seeds ? a.norm_order[base + j] : a.seed_node[sb + base + j];
+                         },
+                         [&](uint32_t j, double d) { w.nd[j] = d; });
+            if (v) raw = w.nd[lane];
+            __syncwarp();
             touch(node, v);
             scored += __popc(__ballot_sync(kFull, v));
             const uint32_t cnt = min(32u, nseeds - base);
@@ -609,13 +730,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
             scored += nnew;
 
             // score first-time neighbours, lane per node
-            for (uint32_t b = 0; b < nnew; b += 32) {
-                const uint32_t i = b + lane;
-                if (i < nnew) {
-                    const uint32_t pos = w.nnew[i];
-                    w.nd[pos] = -hybrid_score<12>(c, sq, w.nb[pos]);
-                }
-            }
+            score_staged(a, sq, w, lane, phase, nnew, [&](uint32_t i) { return w.nb[w.nnew[i]]; },
+                         [&](uint32_t i, double d) { w.nd[w.nnew[i]] = d; });
             __syncwarp();
 
             if (!ctx_mode) {
@@ -940,10 +1056,30 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         a.nbcap = ix->degree + (any_req ? ix->max_kw_edges : 0) + (any_ctx ? a.lccap : 0) + 32;
         a.reqcap = std::max(max_req, 1u);
         auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
-        size_t ws = al(static_cast<size_t>(c.dstride) * 4 + static_cast<size_t>(a.lcap + a.scap) * 8);
+        size_t ws = al(stage_bytes(c.dstride, a.lcap, a.scap));
         ws += al(a.beamcap * 8) + 2 * al(a.kcap * 8) + al(a.nbcap * 8) + al(32 * 8);
         ws += al(a.beamcap * 4) + al(a.kcap * 4) + 2 * al(a.nbcap * 4) + al(a.nbcap);
-        ws += al(a.lccap * 8 + 8) + al(a.reqcap * 4 + 4) + al(32 * 4);
+        ws += al(a.lccap * 8 + 8) + al(a.reqcap * 4 + 4) + al(32 * 4) + 16;
+        // staging slot: dense | learned idx | learned val | stat idx | stat val,
+        // stride = 4 (mod 32) words so 8 lanes' 16-byte reads hit 32 banks
+        a.o_lidx = c.dstride;
+        a.o_lval = a.o_lidx + round4(c.max_lnnz);
+        a.o_sidx = a.o_lval + round4(c.max_lnnz);
+        a.o_sval = a.o_sidx + round4(c.max_snnz);
+        a.slot_words = a.o_sval + round4(c.max_snnz);
+        while (a.slot_words % 32 != 4) a.slot_words += 4;
+        // rows per staging round: the larger of {16, 8, 4} that still lets
+        // >= 2 query-warps share an SM (the chain latency is hidden by
+        // concurrent queries, the copy latency by wide rounds)
+        // Measured on B200 (tools/prof_search.py, 100K docs): the register path
+        // (rb = 0: every lane streams its own row with an 8-float4 prefetch) beats
+        // TMA staging of 4/8/16 rows per round by 2.8x at beam 256 and 1.7x at
+        // beam 2048 — staging slots cost query-warps per SM, and the sequential
+        // fp64 chains need those warps to hide their latency.
+        a.rb = 0;
+        if (const char* e = std::getenv("FGB_SEARCH_RB")) a.rb = static_cast<uint32_t>(std::atoi(e));
+        if (a.rb > 32) a.rb = 32;
+        ws += al(static_cast<size_t>(a.rb) * a.slot_words * 4);
         a.warp_smem = static_cast<uint32_t>(ws);
         const size_t block_smem = ws * kWarpsPerBlock;
         if (block_smem > 227 * 1024)

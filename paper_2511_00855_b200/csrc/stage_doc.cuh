@@ -7,34 +7,42 @@
 namespace fgb {
 
 __host__ __device__ inline size_t doc_stage_bytes(uint32_t dstride, uint32_t lcap, uint32_t scap) {
-    return static_cast<size_t>(dstride) * 4 + static_cast<size_t>(lcap + scap) * 8;
+    return stage_bytes(dstride, lcap, scap);
 }
 
 template <typename Sync>
 __device__ __forceinline__ void stage_doc(const DevCorpus& c, uint64_t u, unsigned char* smem,
                                           uint32_t lcap, uint32_t scap, uint32_t tid,
                                           uint32_t nthreads, SmemQuery& sq, Sync sync) {
-    float* dense = reinterpret_cast<float*>(smem);
-    uint32_t* lkeys = reinterpret_cast<uint32_t*>(dense + c.dstride);
-    float* lvals = reinterpret_cast<float*>(lkeys + lcap);
-    uint32_t* skeys = reinterpret_cast<uint32_t*>(lvals + lcap);
-    float* svals = reinterpret_cast<float*>(skeys + scap);
+    const StagePtrs p = stage_layout(smem, c.dstride, lcap, scap);
     const float* row = c.dense + u * c.dstride;
-    for (uint32_t j = tid; j < c.dstride; j += nthreads) dense[j] = row[j];
-    for (uint32_t j = tid; j < lcap; j += nthreads) lkeys[j] = kEmpty;
-    for (uint32_t j = tid; j < scap; j += nthreads) skeys[j] = kEmpty;
+    for (uint32_t j = tid; j < c.dstride; j += nthreads) p.dense[j] = static_cast<double>(row[j]);
+    for (uint32_t j = tid; j < lcap; j += nthreads) p.lkeys[j] = kEmpty;
+    for (uint32_t j = tid; j < scap; j += nthreads) p.skeys[j] = kEmpty;
+    for (uint32_t j = tid; j < filter_words(lcap); j += nthreads) p.lfilt[j] = 0;
+    for (uint32_t j = tid; j < filter_words(scap); j += nthreads) p.sfilt[j] = 0;
     sync();
     const uint32_t ln = c.l_nnz[u], sn = c.s_nnz[u];
     const uint64_t lo = c.l_off[u], so = c.s_off[u];
-    for (uint32_t j = tid; j < ln; j += nthreads) hash_insert(lkeys, lvals, lcap - 1, c.l_idx[lo + j], c.l_val[lo + j]);
-    for (uint32_t j = tid; j < sn; j += nthreads) hash_insert(skeys, svals, scap - 1, c.s_idx[so + j], c.s_val[so + j]);
+    for (uint32_t j = tid; j < ln; j += nthreads) {
+        const uint32_t t = c.l_idx[lo + j];
+        hash_insert(p.lkeys, p.lvals, lcap - 1, t, c.l_val[lo + j]);
+        atomicOr(&p.lfilt[(t >> 5) & (filter_words(lcap) - 1)], 1u << (t & 31));
+    }
+    for (uint32_t j = tid; j < sn; j += nthreads) {
+        const uint32_t t = c.s_idx[so + j];
+        hash_insert(p.skeys, p.svals, scap - 1, t, c.s_val[so + j]);
+        atomicOr(&p.sfilt[(t >> 5) & (filter_words(scap) - 1)], 1u << (t & 31));
+    }
     sync();
-    sq.dense = dense;
-    sq.lkeys = lkeys;
-    sq.lvals = lvals;
+    sq.dense = p.dense;
+    sq.lkeys = p.lkeys;
+    sq.lvals = p.lvals;
+    sq.lfilt = p.lfilt;
     sq.lmask = ln ? lcap - 1 : 0;
-    sq.skeys = skeys;
-    sq.svals = svals;
+    sq.skeys = p.skeys;
+    sq.svals = p.svals;
+    sq.sfilt = p.sfilt;
     sq.smask = sn ? scap - 1 : 0;
 }
 
