@@ -340,33 +340,34 @@ __device__ int64_t pool_offer(const PoolRef& p, uint32_t& size, double d, uint32
 __device__ uint32_t pool_merge(const PoolRef& p, uint32_t& size, const double* bd,
                                const uint32_t* bn, uint32_t m, uint32_t lane) {
     if (m == 0) return p.cap;
-    uint32_t mypos = p.cap;
+    uint32_t mypos = p.cap, rank = 0xFFFFFFFFu;
     double md = 0;
     uint32_t mn = 0;
     if (lane < m) {
         md = bd[lane];
         mn = bn[lane];
-        mypos = lane + pool_rank(p, size, md, mn);
+        rank = pool_rank(p, size, md, mn);  // # pool entries < new entry `lane`
+        mypos = lane + rank;
     }
+    uint32_t p0 = mypos;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 = min(p0, __shfl_xor_sync(kFull, p0, o));
+    if (p0 >= p.cap) return p.cap;  // every new entry is worse than a full pool
     __syncwarp();
-    if (size > 0) {
-        for (int b = static_cast<int>(((size - 1) / 32) * 32); b >= 0; b -= 32) {
+    // Entries before p0 stay; entry i >= p0 moves right by #{j : rank_j <= i}
+    // (ranks are non-decreasing in j), processed right to left.
+    if (size > p0) {
+        for (int b = static_cast<int>(((size - 1) / 32) * 32); b >= static_cast<int>(p0 & ~31u); b -= 32) {
             const uint32_t i = b + lane;
-            const bool v = i < size;
+            const bool v = i < size && i >= p0;
+            uint32_t shift = 0;
+            for (uint32_t t = 0; t < m; ++t) shift += __shfl_sync(kFull, rank, t) <= i;
             double dd = 0;
-            uint32_t nn = 0, np = p.cap;
+            uint32_t nn = 0;
+            const uint32_t np = i + shift;
             if (v) {
                 dd = p.d[i];
                 nn = p.n[i];
-                uint32_t lo = 0, hi = m;  // # new entries < pool[i]
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (eless(bd[mid], bn[mid], dd, nn & kNodeMask))
-                        lo = mid + 1;
-                    else
-                        hi = mid;
-                }
-                np = i + lo;
             }
             __syncwarp();
             if (v && np < p.cap) {
