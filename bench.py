@@ -116,41 +116,14 @@ def peak_hbm():
 
 
 def dist_setup(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2511_00855_b200.shard import env_world
+    world, rank, local = env_world()
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
-
-
-def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-
-
-def allmax(world, x):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([float(x)], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
-def bcast(world, x):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([float(x)], device="cuda")
-    dist.broadcast(t, 0)
-    return t.item()
 
 
 def flush_l2(local):
@@ -177,8 +150,10 @@ def main():
 
     from paper_2511_00855_b200 import _abi as A, fusegraph as fg, synth
     import torch
+    from paper_2511_00855_b200.shard import Group, shard_range
 
     torch.cuda.set_device(local)
+    group = Group(world, device=f"cuda:{local}")
     t0 = time.time()
     p = synth_params(args.docs)
     corpus, kg, _ = synth.generate_corpus(p, 0)
@@ -205,11 +180,10 @@ def main():
                 break
         best = next((s for s in sweep if s["recall"] >= 0.9), max(sweep, key=lambda s: s["recall"]))
         beam = best["beam"]
-    beam = int(bcast(world, beam))
+    beam = int(group.bcast(beam))
 
     # ---- this rank's shard
-    per = (queries.count + world - 1) // world
-    lo, hi = rank * per, min(queries.count, (rank + 1) * per)
+    lo, hi = shard_range(queries.count, world, rank)
     shard = queries.subset(np.arange(lo, hi)).with_(beam_width=max(beam, 10))
     for _ in range(args.warmup):
         fg.batch_query(ix, shard)
@@ -218,7 +192,7 @@ def main():
     kern_ms, wall_s, scored, expanded = [], [], 0, 0
     for _ in range(args.steps):
         flush_l2(local)
-        barrier(world)
+        group.barrier()
         torch.cuda.synchronize(local)
         t0 = time.perf_counter()
         r = fg.batch_query(ix, shard)  # H2D queries + kernel + D2H hits
@@ -228,9 +202,9 @@ def main():
         kern_ms.append(ms)
         scored, expanded = int(r.scored.sum()), int(r.expanded.sum())
     clk = clocks.stop()
-    barrier(world)
-    k_tot = allmax(world, sum(kern_ms) / 1e3)
-    w_tot = allmax(world, sum(wall_s))
+    group.barrier()
+    k_tot = group.max(sum(kern_ms) / 1e3)
+    w_tot = group.max(sum(wall_s))
     n_total = queries.count * args.steps
     value = n_total / k_tot
     e2e = n_total / w_tot
