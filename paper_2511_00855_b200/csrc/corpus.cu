@@ -12,12 +12,13 @@ namespace {
 
 // finalize_fused (types.cpp:74-79): dense self-dot, then learned, then
 // statistical self sparse dot (every term shared, ascending order).
-__global__ void sqnorm_kernel(DevCorpus c, double* out) {
+__global__ void sqnorm_kernel(DevCorpus c, double* out, double* dnorm) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= c.n) return;
     const float* row = c.dense + i * c.dstride;
     double acc = 0.0;
     for (uint32_t j = 0; j < c.dim; ++j) acc = __fma_rn((double)row[j], (double)row[j], acc);
+    dnorm[i] = sqrt(acc);
     double l = 0.0;
     for (uint32_t j = 0; j < c.l_nnz[i]; ++j) {
         const double v = c.l_val[c.l_off[i] + j];
@@ -246,6 +247,7 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             for (uint64_t i = 0; i < n; ++i) c->deleted_h[i] = v->deleted[i] ? 1 : 0;
         c->deleted.upload(c->deleted_h, s);
         c->sqnorm.alloc(n);
+        c->dnorm.alloc(n);
 
         c->dc = DevCorpus{n,
                           c->dim,
@@ -264,8 +266,9 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
                           c->ent_ptr.get(),
                           c->ent_idx.get(),
                           c->sqnorm.get(),
+                          c->dnorm.get(),
                           c->deleted.get()};
-        sqnorm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->sqnorm.get());
+        sqnorm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->sqnorm.get(), c->dnorm.get());
         FGB_LAUNCH("sqnorm_kernel");
         c->sqnorm_h.resize(n);
         c->sqnorm.download(c->sqnorm_h.data(), n, s);

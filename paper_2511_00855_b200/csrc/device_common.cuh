@@ -45,6 +45,7 @@ struct DevCorpus {
     const uint64_t* ent_ptr;
     const uint32_t* ent_idx;
     const double* sqnorm;
+    const double* dnorm;  // sqrt of the dense self-dot (screening bounds only)
     const uint8_t* deleted;
 };
 
@@ -270,6 +271,47 @@ __device__ __forceinline__ double hybrid_score(const DevCorpus& c, const SmemQue
                                                 q.skeys, q.svals, q.smask, q.sfilt)
                                  : 0.0);
     return acc;
+}
+
+// Exact-score screening.  For a candidate whose sparse parts L, S are known,
+// the final computed score RN(RN(D + L) + S) (D = the dense chain) is at most
+//   L + S + |q||d| + 1e-11 (|q||d| + |L| + |S|)
+// (the chain's rounding error is <= d * 2^-53 * sum|q_i d_i| <= 1e-13 |q||d|
+// for d <= 9000, two more roundings add 2^-52 relative; the margin covers the
+// norms' own rounding).  A candidate whose bound is below a threshold score
+// can never beat it, so its 4*d-byte dense row is never read.
+__device__ __forceinline__ double score_upper_bound(double qn, double dn, double l, double s) {
+    const double qd = qn * dn;
+    return l + s + qd + 1e-11 * (qd + fabs(l) + fabs(s)) + 1e-300;
+}
+
+__device__ __forceinline__ double sparse_part(const DevCorpus& c, const SmemQuery& q, uint64_t node,
+                                              bool learned) {
+    if (learned)
+        return q.lmask ? sparse_chain(c.l_idx, c.l_val, c.l_off[node], c.l_nnz[node], q.lkeys, q.lvals,
+                                      q.lmask, q.lfilt)
+                       : 0.0;
+    return q.smask ? sparse_chain(c.s_idx, c.s_val, c.s_off[node], c.s_nnz[node], q.skeys, q.svals,
+                                  q.smask, q.sfilt)
+                   : 0.0;
+}
+
+// hybrid_score with screening: returns false (and no score) when the upper
+// bound is < `floor`; otherwise the exact, bit-identical score in `out`.
+// Partial sums are combined in the reference's order (dense + learned, then
+// + statistical), so the result equals hybrid_score exactly.
+template <uint32_t kStage = 8>
+__device__ __forceinline__ bool hybrid_score_screened(const DevCorpus& c, const SmemQuery& q,
+                                                      uint64_t node, double qnorm, double floor,
+                                                      double& out) {
+    const double l = sparse_part(c, q, node, true);
+    const double s = sparse_part(c, q, node, false);
+    if (q.dense && score_upper_bound(qnorm, c.dnorm[node], l, s) < floor) return false;
+    if (!q.dense && score_upper_bound(0.0, 0.0, l, s) < floor) return false;
+    double acc = q.dense ? dense_chain<kStage>(c, q.dense, node) : 0.0;
+    acc = __dadd_rn(acc, l);
+    out = __dadd_rn(acc, s);
+    return true;
 }
 
 // Sorted-list membership (sorted_contains, types.cpp:86-88).

@@ -114,7 +114,7 @@ struct fg_corpus {
     fgb::DevBuf<float> dense, l_val, s_val;
     fgb::DevBuf<uint64_t> l_off, s_off, kw_ptr, ent_ptr;
     fgb::DevBuf<uint32_t> l_nnz, s_nnz, l_idx, s_idx, kw_idx, ent_idx;
-    fgb::DevBuf<double> sqnorm;
+    fgb::DevBuf<double> sqnorm, dnorm;
     fgb::DevBuf<uint8_t> deleted;
     // host copies used by host-side stages (entity map, logical edges, seeds)
     std::vector<uint64_t> doc_id;

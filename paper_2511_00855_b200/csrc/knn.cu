@@ -210,13 +210,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     __syncthreads();
 
     // Score fresh, new candidates; merge survivors into the running top-k.
+    const double unorm = a.c.dnorm[u];
     for (uint32_t base = 0; base < a.pool_cap; base += nt) {
         const uint32_t s = base + tid;
         const uint32_t id = s < a.pool_cap ? keys[s] : kEmpty;
         const bool cand = id != kEmpty && ((fbits[s >> 5] >> (s & 31)) & 1u) &&
                           !((hbits[s >> 5] >> (s & 31)) & 1u);
-        if (cand) {
-            const double sc = hybrid_score(a.c, sq, id);
+        double sc;
+        // screened: candidates whose exact-score upper bound (sparse parts +
+        // |u||v|) is below the running k-th score never read their dense row
+        if (cand && hybrid_score_screened(a.c, sq, id, unorm, T_sc[k - 1], sc)) {
             if (better(sc, id, T_sc[k - 1], T_id[k - 1])) {
                 const uint32_t slot = atomicAdd(&S_cnt, 1u);
                 S_sc[slot] = sc;

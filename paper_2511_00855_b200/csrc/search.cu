@@ -152,11 +152,18 @@ __device__ WarpMem carve(unsigned char* base, const SearchArgs& a) {
 template <typename NodeOf, typename Sink>
 __device__ void score_staged(const SearchArgs& a, const SmemQuery& sq, const WarpMem& w,
                              uint32_t lane, uint32_t& phase, uint32_t count, NodeOf node_of,
-                             Sink sink) {
+                             Sink sink, double qnorm = 0.0,
+                             double floor = -__builtin_huge_val()) {
     const DevCorpus& c = a.c;
     if (a.rb == 0) {  // register path: each lane streams its own row
         for (uint32_t b = 0; b < count; b += 32) {
-            if (b + lane < count) sink(b + lane, -hybrid_score<12>(c, sq, node_of(b + lane)));
+            if (b + lane < count) {
+                // screened: a node whose exact-score bound cannot reach either
+                // full pool's worst entry gets +inf (never offered, never read)
+                double s;
+                const bool scored = hybrid_score_screened<8>(c, sq, node_of(b + lane), qnorm, floor, s);
+                sink(b + lane, scored ? -s : __longlong_as_double(0x7FF0000000000000ll));
+            }
         }
         __syncwarp();
         return;
@@ -357,11 +364,23 @@ __device__ uint32_t pool_merge(const PoolRef& p, uint32_t& size, const double* b
     // Entries before p0 stay; entry i >= p0 moves right by #{j : rank_j <= i}
     // (ranks are non-decreasing in j), processed right to left.
     if (size > p0) {
+        // ranks to shared memory (the sorted bn slots are no longer needed)
+        uint32_t* br = const_cast<uint32_t*>(bn);
+        __syncwarp();
+        if (lane < m) br[lane] = rank;
+        __syncwarp();
         for (int b = static_cast<int>(((size - 1) / 32) * 32); b >= static_cast<int>(p0 & ~31u); b -= 32) {
             const uint32_t i = b + lane;
             const bool v = i < size && i >= p0;
-            uint32_t shift = 0;
-            for (uint32_t t = 0; t < m; ++t) shift += __shfl_sync(kFull, rank, t) <= i;
+            uint32_t lo = 0, hi = m;  // shift = #{j : rank_j <= i} (upper bound)
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (br[mid] <= i)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            const uint32_t shift = lo;
             double dd = 0;
             uint32_t nn = 0;
             const uint32_t np = i + shift;
@@ -498,6 +517,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
         const bool ctx_mode = (flags & QF_ENTITY) != 0;
         SmemQuery sq;
         stage_query(a.q, qi, c.dstride, w.stage, a.lcap, a.scap, lane, 32, sq, [] { __syncwarp(); });
+        double qnorm = 0.0;  // |weighted query dense| for the screening bound
+        if (sq.dense) {
+            for (uint32_t j = lane; j < c.dstride; j += 32) qnorm += sq.dense[j] * sq.dense[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) qnorm += __shfl_xor_sync(kFull, qnorm, o);
+            qnorm = sqrt(qnorm) * (1.0 + 1e-12);
+        }
         const uint64_t rb = a.q.req_ptr[qi];
         const uint32_t R = static_cast<uint32_t>(a.q.req_ptr[qi + 1] - rb);
         for (uint32_t i = lane; i < R; i += 32) w.req[i] = a.q.req_idx[rb + i];
@@ -730,9 +756,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
             nbc = nkeep;
             scored += nnew;
 
-            // score first-time neighbours, lane per node
+            // score first-time neighbours, lane per node.  Plain queries screen
+            // against the worst entries of BOTH pools when both are full (an
+            // offer below both is a no-op); entity-context queries may re-offer
+            // a node later with a better distance, so they always score.
+            double floor = -__longlong_as_double(0x7FF0000000000000ll);
+            if (!ctx_mode && csize == B && tsize == K)
+                floor = fmin(-w.cand_d[csize - 1], -w.topk_d[tsize - 1]);
             score_staged(a, sq, w, lane, phase, nnew, [&](uint32_t i) { return w.nb[w.nnew[i]]; },
-                         [&](uint32_t i, double d) { w.nd[w.nnew[i]] = d; });
+                         [&](uint32_t i, double d) { w.nd[w.nnew[i]] = d; }, qnorm, floor);
             __syncwarp();
 
             if (!ctx_mode) {
