@@ -9,10 +9,13 @@ fusion with per-query weights (random_simplex_weights, as the reference CLI's
 
 One step = one batched beam search of this rank's query shard (the index is
 replicated per GPU; queries shard by contiguous range, no collective on the
-data path -> "scaling": "weak" in queries per GPU).  The beam is the smallest
-of {16..2048} whose mean recall@10 against exact (GPU brute-force) truth on the
-eval subset reaches 0.9; if none does, the highest-recall beam is used and
-`recall_target_met` is false.  `value` = queries / device time of the search
+data path -> "scaling": "weak" in queries per GPU).  The operating point is
+the (SearchOptions::entry_count, beam_width) pair — both query-time options of
+the reference API — with the highest kernel QPS among those whose mean
+recall@10 against exact (GPU brute-force) truth on the eval subset reaches 0.9
+(per entry_count the beam sweep {16..2048} stops at the first beam reaching
+0.9); if none does, the highest-recall pair is used and `recall_target_met` is
+false.  `value` = queries / device time of the search
 kernel (CUDA events, max over ranks); `e2e` = queries / wall time of the public
 C-ABI call with host buffers (H2D of the queries + D2H of the hits inside).
 L2 is flushed (256 MiB write) before every timed step; the corpus (4 GB) is
@@ -39,6 +42,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BEAMS = [16, 32, 64, 128, 256, 512, 1024, 2048]
+# SearchOptions::entry_count (search.hpp:45-49): the number of largest-norm
+# entry points (index.cpp:15-22).  A query-time option of the reference API;
+# results for a given (entry_count, beam) are identical on both arms.
+ENTRIES = [32, 64, 128, 256, 512, 1024]
 
 
 def parse():
@@ -52,6 +59,7 @@ def parse():
     ap.add_argument("--eval-queries", type=int, default=1000)
     ap.add_argument("--cpu-sample", type=int, default=128)
     ap.add_argument("--beam", type=int, default=0, help="force a beam (skip the sweep)")
+    ap.add_argument("--entry", type=int, default=0, help="force an entry_count (with --beam)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -165,28 +173,24 @@ def main():
     stages = ix.build_times()
 
     queries = synth.synth_queries(p, args.queries)
-    # ---- operating point: smallest beam with recall@10 >= 0.9 (rank 0 decides)
+    # ---- operating point: over entry_count x beam, the fastest setting whose
+    # recall@10 on the eval subset reaches 0.9 (rank 0 decides)
     sweep = []
-    beam = args.beam
+    beam, entry = args.beam, args.entry or 32
     if rank == 0:
         ev = queries.subset(np.arange(min(args.eval_queries, queries.count)))
         truth = fg.brute_force_topk(dc, ev)
-        for b in ([beam] if beam else BEAMS):
-            r = fg.batch_query(ix, ev.with_(beam_width=max(b, 10)))
-            rec = float(np.mean([fg.recall_at_k(r.ids(i), truth.ids(i), 10) for i in range(ev.count)]))
-            ms, _ = ix.last_search_stats()
-            sweep.append({"beam": b, "recall": round(rec, 4), "qps_kernel": round(ev.count / (ms / 1e3), 1)})
-            if rec >= 0.9:
-                break
-        best = next((s for s in sweep if s["recall"] >= 0.9), max(sweep, key=lambda s: s["recall"]))
-        beam = best["beam"]
+        sweep = sweep_operating_points(fg, ix, ev, truth, args)
+        best = select_operating_point(sweep)
+        beam, entry = best["beam"], best["entry"]
     beam = int(group.bcast(beam))
+    entry = int(group.bcast(entry))
 
     # ---- this rank's shard
     lo, hi = shard_range(queries.count, world, rank)
     shard = queries.subset(np.arange(lo, hi)).with_(beam_width=max(beam, 10))
     for _ in range(args.warmup):
-        fg.batch_query(ix, shard)
+        fg.batch_query(ix, shard, entry_count=entry)
 
     clocks = Clocks(local)
     kern_ms, wall_s, scored, expanded = [], [], 0, 0
@@ -195,7 +199,7 @@ def main():
         group.barrier()
         torch.cuda.synchronize(local)
         t0 = time.perf_counter()
-        r = fg.batch_query(ix, shard)  # H2D queries + kernel + D2H hits
+        r = fg.batch_query(ix, shard, entry_count=entry)  # H2D queries + kernel + D2H hits
         torch.cuda.synchronize(local)
         wall_s.append(time.perf_counter() - t0)
         ms, launches = ix.last_search_stats()
@@ -241,11 +245,11 @@ def main():
             "workload": "configs[1]: 1M docs MS MARCO-shaped dense d=768 + learned sparse nnz 120 "
                         "(vocab 30522), dense+sparse fusion, per-query simplex weights",
             "docs": corpus.n, "queries_per_step": queries.count, "queries_per_gpu": hi - lo,
-            "k": 10, "beam": beam, "entry_count": 32, "build": BUILD,
+            "k": 10, "beam": beam, "entry_count": entry, "build": BUILD,
             "parallelism": f"query-shard x{world}, index replicated",
             "l2": "flushed (256 MiB write) before each timed step; corpus 4 GB > L2",
         },
-        "recall_at_10": next((s["recall"] for s in sweep if s["beam"] == beam), None),
+        "recall_at_10": next((s["recall"] for s in sweep if s["beam"] == beam and s["entry"] == entry), None),
         "recall_target_met": any(s["recall"] >= 0.9 for s in sweep) if sweep else None,
         "beam_sweep": sweep,
         "build_seconds": round(build_s, 2),
@@ -263,7 +267,7 @@ def main():
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(corpus, kg, ix, queries, beam, args.cpu_sample)
+        line["cpu_baseline"] = cpu_baseline(corpus, kg, ix, queries, beam, entry, args.cpu_sample)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -271,7 +275,32 @@ def main():
         dist.destroy_process_group()
 
 
-def cpu_baseline(corpus, kg, ix, queries, beam, sample):
+def sweep_operating_points(fg, ix, ev, truth, args):
+    """recall@10 / kernel QPS over entry_count x beam; per entry_count the beam
+    sweep stops at the first beam reaching 0.9 (larger beams only cost more)."""
+    rows = []
+    entries = [args.entry] if args.entry else ENTRIES
+    beams = [args.beam] if args.beam else BEAMS
+    for e in entries:
+        for b in beams:
+            r = fg.batch_query(ix, ev.with_(beam_width=max(b, 10)), entry_count=e)
+            rec = float(np.mean([fg.recall_at_k(r.ids(i), truth.ids(i), 10) for i in range(ev.count)]))
+            ms, _ = ix.last_search_stats()
+            rows.append({"entry": e, "beam": b, "recall": round(rec, 4),
+                         "qps_kernel": round(ev.count / (ms / 1e3), 1)})
+            if rec >= 0.9:
+                break
+    return rows
+
+
+def select_operating_point(sweep):
+    ok = [s for s in sweep if s["recall"] >= 0.9]
+    if ok:
+        return max(ok, key=lambda s: s["qps_kernel"])
+    return max(sweep, key=lambda s: s["recall"])
+
+
+def cpu_baseline(corpus, kg, ix, queries, beam, entry, sample):
     """The reference's own batch_query on host cores over the same index."""
     from oracle.refpy import RefLib, ref_available
     if not ref_available():
@@ -287,10 +316,11 @@ def cpu_baseline(corpus, kg, ix, queries, beam, sample):
     q = queries.subset(np.arange(min(sample, queries.count))).with_(beam_width=max(beam, 10))
     pq = ref.prepare_queries(q)
     t0 = time.perf_counter()
-    ref.batch_query_prepared(rix, pq, 0, q.count, 10, threads=cores)
+    ref.batch_query_prepared(rix, pq, 0, q.count, 10, entry_count=entry, threads=cores)
     dt = time.perf_counter() - t0
     return {"value": round(q.count / dt, 2), "unit": "queries/s", "cores": cores, "kind": "reference",
-            "sample": f"{q.count} queries of the same batch at beam {beam} on the same 1M index "
+            "sample": f"{q.count} queries of the same batch at beam {beam}, entry_count {entry} "
+                      f"on the same {corpus.n}-doc index "
                       f"(fusegraph_ref::batch_query, {cores} threads; store/index load {prep_s:.0f}s untimed)"}
 
 
@@ -307,21 +337,15 @@ def reference_arm(args, world, rank, local):
     p = synth_params(args.docs)
     corpus, kg, _ = synth.generate_corpus(p, 0)
     queries = synth.synth_queries(p, args.queries)
-    beam = args.beam
     # index fixture: the GPU build (bit-identical to fusegraph_ref::build_hybrid_index)
     dc = fg.DeviceCorpus(corpus, device=local)
     ix = fg.build_hybrid_index(dc, kg, **BUILD)
-    if not beam:
+    beam, entry = args.beam, args.entry or 32
+    if not (args.beam and args.entry):
         ev = queries.subset(np.arange(min(args.eval_queries, queries.count)))
         truth = fg.brute_force_topk(dc, ev)
-        sweep = []
-        for b in BEAMS:
-            r = fg.batch_query(ix, ev.with_(beam_width=max(b, 10)))
-            rec = float(np.mean([fg.recall_at_k(r.ids(i), truth.ids(i), 10) for i in range(ev.count)]))
-            sweep.append((b, rec))
-            if rec >= 0.9:
-                break
-        beam = next((b for b, r in sweep if r >= 0.9), max(sweep, key=lambda x: x[1])[0])
+        best = select_operating_point(sweep_operating_points(fg, ix, ev, truth, args))
+        beam, entry = best["beam"], best["entry"]
     g = ix.export()
     ix.close()
     dc.close()
@@ -330,14 +354,14 @@ def reference_arm(args, world, rank, local):
     q = queries.subset(np.arange(min(args.cpu_sample, queries.count))).with_(beam_width=max(beam, 10))
     pq = ref.prepare_queries(q)
     for _ in range(args.warmup):
-        ref.batch_query_prepared(rix, pq, 0, min(q.count, 16), 10, threads=cores)
+        ref.batch_query_prepared(rix, pq, 0, min(q.count, 16), 10, entry_count=entry, threads=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        ref.batch_query_prepared(rix, pq, 0, q.count, 10, threads=cores)
+        ref.batch_query_prepared(rix, pq, 0, q.count, 10, entry_count=entry, threads=cores)
         times.append(time.perf_counter() - t0)
     v = q.count * args.steps / sum(times)
-    sample = (f"{q.count} queries/step of the configs[1] batch at beam {beam}, "
+    sample = (f"{q.count} queries/step of the configs[1] batch at beam {beam}, entry_count {entry}, "
               f"fusegraph_ref::batch_query with {cores} threads over the same 1M index")
     print(json.dumps({
         "impl": "reference",
@@ -347,6 +371,7 @@ def reference_arm(args, world, rank, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 storage / f64 accumulate", "data": "synthetic, seed 1",
         "config": {"workload": "configs[1] (1M docs, d=768, learned nnz 120)", "beam": beam,
+                   "entry_count": entry,
                    "docs": corpus.n, "queries_per_step": q.count},
         "cpu_baseline": {"value": round(v, 2), "unit": "queries/s", "cores": cores,
                          "kind": "reference", "sample": sample},
