@@ -13,7 +13,9 @@ import os
 from . import _abi as A
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfgb200.so")
+# FGB_LIB_VARIANT=x loads libfgb200.x.so (dev A/B builds of the same sources)
+_VAR = os.environ.get("FGB_LIB_VARIANT")
+LIB_PATH = os.path.join(_HERE, f"libfgb200.{_VAR}.so" if _VAR else "libfgb200.so")
 
 
 class Error(RuntimeError):

@@ -54,6 +54,14 @@ __device__ double sparse_merge(const uint32_t* idx, const float* val, uint64_t o
     return acc;
 }
 
+// Packed per-node gather record (DevCorpus::meta).
+__global__ void meta_kernel(DevCorpus c, const double* dnorm, uint4* meta) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= c.n) return;
+    meta[i] = make_uint4(static_cast<uint32_t>(c.l_off[i] >> 2), static_cast<uint32_t>(c.s_off[i] >> 2),
+                         c.l_nnz[i] | (c.s_nnz[i] << 16), __float_as_uint(__double2float_ru(dnorm[i])));
+}
+
 __global__ void pair_kernel(DevCorpus c, const uint32_t* a, const uint32_t* b, uint64_t m,
                             double* out) {
     const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -210,12 +218,14 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             std::vector<uint32_t> nnz, idx;
             std::vector<float> val;
             build_sparse(v->learned, n, off, nnz, idx, val, c->max_lnnz, "learned");
+            c->l_nnz_total4 = idx.size() / 4;
             c->l_off.upload(off, s);
             c->l_nnz.upload(nnz, s);
             c->l_idx.upload(idx.empty() ? std::vector<uint32_t>(4, kPad) : idx, s);
             c->l_val.upload(val.empty() ? std::vector<float>(4, 0.f) : val, s);
             FGB_CUDA(cudaStreamSynchronize(s));
             build_sparse(v->statistical, n, off, nnz, idx, val, c->max_snnz, "statistical");
+            c->s_nnz_total4 = idx.size() / 4;
             c->s_off.upload(off, s);
             c->s_nnz.upload(nnz, s);
             c->s_idx.upload(idx.empty() ? std::vector<uint32_t>(4, kPad) : idx, s);
@@ -267,12 +277,23 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
                           c->ent_idx.get(),
                           c->sqnorm.get(),
                           c->dnorm.get(),
-                          c->deleted.get()};
+                          c->deleted.get(),
+                          nullptr};
         sqnorm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->sqnorm.get(), c->dnorm.get());
         FGB_LAUNCH("sqnorm_kernel");
+        // offsets / 4 must fit 32 bits and nnz 16 bits for the packed record
+        const uint64_t l_end = c->l_nnz_total4, s_end = c->s_nnz_total4;
+        if (c->max_lnnz < 65536 && c->max_snnz < 65536 && l_end < (1ull << 32) && s_end < (1ull << 32)) {
+            c->meta.alloc(n);
+            meta_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->dnorm.get(), c->meta.get());
+            FGB_LAUNCH("meta_kernel");
+            c->dc.meta = c->meta.get();
+        }
         c->sqnorm_h.resize(n);
         c->sqnorm.download(c->sqnorm_h.data(), n, s);
         FGB_CUDA(cudaStreamSynchronize(s));
+        c->max_sqnorm = 0.0;
+        for (double x : c->sqnorm_h) c->max_sqnorm = std::max(c->max_sqnorm, x);
         *out = c.release();
     });
 }

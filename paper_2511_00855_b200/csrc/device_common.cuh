@@ -47,6 +47,10 @@ struct DevCorpus {
     const double* sqnorm;
     const double* dnorm;  // sqrt of the dense self-dot (screening bounds only)
     const uint8_t* deleted;
+    // packed per-node record for one-load gathers (nullptr when a row has
+    // >= 65,536 postings): x = l_off / 4, y = s_off / 4,
+    // z = l_nnz | s_nnz << 16, w = bits of float(dnorm) rounded up
+    const uint4* meta;
 };
 
 // ---------------------------------------------------------------- hashing
@@ -146,6 +150,13 @@ __device__ __forceinline__ StagePtrs stage_layout(unsigned char* smem, uint32_t 
 }
 
 // Dense dot of the staged query against row `node`, sequential over i.
+//
+// Each step is acc = RN(acc + p_i) with p_i = q_i * d_i computed by DMUL: the
+// product of two fp32 values widened to fp64 is EXACT, so RN(acc + p_i) is
+// the same rounding as the reference's `acc += a * b` (one rounding of the
+// exact a*b + acc).  On B200 a DADD chain has a shorter dependent latency and
+// twice the issue rate of a DFMA chain (tools/ubench_chain.cu: 10.2 vs 11.5
+// cycles/element, 21.6 vs 16 elements/clk/SM), and the DMULs sit off the chain.
 template <uint32_t kStage = 8>
 __device__ __forceinline__ double dense_chain(const DevCorpus& c, const double* q, uint64_t node) {
     // Software-pipelined: the next kStage float4 of the row are in flight
@@ -155,6 +166,26 @@ __device__ __forceinline__ double dense_chain(const DevCorpus& c, const double* 
     const uint32_t n4 = c.dstride >> 2;
     double acc = 0.0;
     float4 cur[kStage], nxt[kStage];
+    if (n4 % kStage == 0) {  // d = 128, 768, ...: no per-element guards
+#pragma unroll
+        for (uint32_t j = 0; j < kStage; ++j) cur[j] = __ldg(row + j);
+        for (uint32_t i = 0; i < n4; i += kStage) {
+            const bool more = i + kStage < n4;
+#pragma unroll
+            for (uint32_t j = 0; j < kStage; ++j) nxt[j] = more ? __ldg(row + i + kStage + j) : cur[j];
+#pragma unroll
+            for (uint32_t j = 0; j < kStage; ++j) {
+                const double2 a = q2[2 * (i + j)], b = q2[2 * (i + j) + 1];
+                acc = __dadd_rn(acc, __dmul_rn(a.x, (double)cur[j].x));
+                acc = __dadd_rn(acc, __dmul_rn(a.y, (double)cur[j].y));
+                acc = __dadd_rn(acc, __dmul_rn(b.x, (double)cur[j].z));
+                acc = __dadd_rn(acc, __dmul_rn(b.y, (double)cur[j].w));
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < kStage; ++j) cur[j] = nxt[j];
+        }
+        return acc;
+    }
 #pragma unroll
     for (uint32_t j = 0; j < kStage; ++j) cur[j] = j < n4 ? __ldg(row + j) : make_float4(0, 0, 0, 0);
     for (uint32_t i = 0; i < n4; i += kStage) {
@@ -165,10 +196,10 @@ __device__ __forceinline__ double dense_chain(const DevCorpus& c, const double* 
         for (uint32_t j = 0; j < kStage; ++j) {
             if (i + j < n4) {
                 const double2 a = q2[2 * (i + j)], b = q2[2 * (i + j) + 1];
-                acc = __fma_rn(a.x, (double)cur[j].x, acc);
-                acc = __fma_rn(a.y, (double)cur[j].y, acc);
-                acc = __fma_rn(b.x, (double)cur[j].z, acc);
-                acc = __fma_rn(b.y, (double)cur[j].w, acc);
+                acc = __dadd_rn(acc, __dmul_rn(a.x, (double)cur[j].x));
+                acc = __dadd_rn(acc, __dmul_rn(a.y, (double)cur[j].y));
+                acc = __dadd_rn(acc, __dmul_rn(b.x, (double)cur[j].z));
+                acc = __dadd_rn(acc, __dmul_rn(b.y, (double)cur[j].w));
             }
         }
 #pragma unroll
@@ -257,6 +288,24 @@ __device__ __forceinline__ void prefetch_row(const DevCorpus& c, const SmemQuery
     }
 }
 
+// Sparse spans only (the dense row is fetched after screening decides).
+__device__ __forceinline__ void prefetch_sparse(const DevCorpus& c, const SmemQuery& q, uint64_t node) {
+    if (q.lmask) {
+        const uint32_t b = ((c.l_nnz[node] + 3) & ~3u) * 4;
+        if (b) {
+            l2_prefetch(c.l_idx + c.l_off[node], b);
+            l2_prefetch(c.l_val + c.l_off[node], b);
+        }
+    }
+    if (q.smask) {
+        const uint32_t b = ((c.s_nnz[node] + 3) & ~3u) * 4;
+        if (b) {
+            l2_prefetch(c.s_idx + c.s_off[node], b);
+            l2_prefetch(c.s_val + c.s_off[node], b);
+        }
+    }
+}
+
 // hybrid_score(weighted query, doc) (scoring.cpp:88-99): dense, then learned,
 // then statistical, in that fixed order.
 template <uint32_t kStage = 8>
@@ -308,6 +357,9 @@ __device__ __forceinline__ bool hybrid_score_screened(const DevCorpus& c, const 
     const double s = sparse_part(c, q, node, false);
     if (q.dense && score_upper_bound(qnorm, c.dnorm[node], l, s) < floor) return false;
     if (!q.dense && score_upper_bound(0.0, 0.0, l, s) < floor) return false;
+    // the whole row toward L2 in one bulk request: only the first stage of
+    // the chain below waits for DRAM
+    if (q.dense) l2_prefetch(c.dense + node * c.dstride, c.dstride * 4);
     double acc = q.dense ? dense_chain<kStage>(c, q.dense, node) : 0.0;
     acc = __dadd_rn(acc, l);
     out = __dadd_rn(acc, s);

@@ -110,17 +110,20 @@ struct fg_corpus {
     uint64_t n = 0;
     uint32_t dim = 0, dstride = 0;
     uint32_t max_lnnz = 0, max_snnz = 0;
+    uint64_t l_nnz_total4 = 0, s_nnz_total4 = 0;  // padded posting counts / 4
     fgb::DevCorpus dc{};
     fgb::DevBuf<float> dense, l_val, s_val;
     fgb::DevBuf<uint64_t> l_off, s_off, kw_ptr, ent_ptr;
     fgb::DevBuf<uint32_t> l_nnz, s_nnz, l_idx, s_idx, kw_idx, ent_idx;
     fgb::DevBuf<double> sqnorm, dnorm;
+    fgb::DevBuf<uint4> meta;
     fgb::DevBuf<uint8_t> deleted;
     // host copies used by host-side stages (entity map, logical edges, seeds)
     std::vector<uint64_t> doc_id;
     std::vector<uint8_t> deleted_h;
     fgb::HostList keywords, entities;
     std::vector<double> sqnorm_h;
+    double max_sqnorm = 0.0;  // max over docs of the unit-weight self score (error bounds)
     cudaStream_t stream = nullptr;
 };
 

@@ -25,6 +25,7 @@
 //    single-entry offers (exactly Pool::offer, search.cpp:26-42).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -32,6 +33,7 @@
 #include "fg_cuda.hpp"
 #include "index.hpp"
 #include "query_stage.cuh"
+#include "search_plain.hpp"
 #include "tma.cuh"
 
 namespace fgb {
@@ -90,6 +92,17 @@ struct SearchArgs {
     uint32_t* r_warn;
     uint32_t* r_err;
     unsigned int* work;
+    // optional phase timing (FGB_SEARCH_TIMING=1): clock64 cycles summed over
+    // warps per phase, see kPhase* below
+    unsigned long long* timing;
+    int prefetch;  // L2 row prefetch of first-time neighbours (FGB_SEARCH_PREFETCH, default on)
+};
+
+// Phase-timing slots (warp-level cycles unless noted)
+enum : int {
+    kPhSeeds = 0, kPhSelect, kPhAdj, kPhDedupe, kPhScore, kPhMerge, kPhFinal,
+    kPhLaneSparse, kPhLaneDense, kPhLaneScored, kPhLaneDenseRows, kPhQueries, kPhExpanded,
+    kPhCount
 };
 
 __device__ __forceinline__ bool eless(double d1, uint32_t n1, double d2, uint32_t n2) {
@@ -161,7 +174,28 @@ __device__ void score_staged(const SearchArgs& a, const SmemQuery& sq, const War
                 // screened: a node whose exact-score bound cannot reach either
                 // full pool's worst entry gets +inf (never offered, never read)
                 double s;
-                const bool scored = hybrid_score_screened<8>(c, sq, node_of(b + lane), qnorm, floor, s);
+                bool scored;
+                if (a.timing) {
+                    const uint32_t node = node_of(b + lane);
+                    const long long t0 = clock64();
+                    const double l = sparse_part(c, sq, node, true);
+                    const double sp = sparse_part(c, sq, node, false);
+                    const long long t1 = clock64();
+                    scored = !(score_upper_bound(sq.dense ? qnorm : 0.0, sq.dense ? c.dnorm[node] : 0.0, l, sp) < floor);
+                    if (scored) {
+                        if (sq.dense) l2_prefetch(c.dense + (uint64_t)node * c.dstride, c.dstride * 4);
+                        double acc = sq.dense ? dense_chain<8>(c, sq.dense, node) : 0.0;
+                        acc = __dadd_rn(acc, l);
+                        s = __dadd_rn(acc, sp);
+                    }
+                    const long long t2 = clock64();
+                    atomicAdd(&a.timing[kPhLaneSparse], (unsigned long long)(t1 - t0));
+                    atomicAdd(&a.timing[kPhLaneDense], (unsigned long long)(t2 - t1));
+                    atomicAdd(&a.timing[kPhLaneScored], 1ull);
+                    if (scored) atomicAdd(&a.timing[kPhLaneDenseRows], 1ull);
+                } else {
+                    scored = hybrid_score_screened<8>(c, sq, node_of(b + lane), qnorm, floor, s);
+                }
                 sink(b + lane, scored ? -s : __longlong_as_double(0x7FF0000000000000ll));
             }
         }
@@ -496,6 +530,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
     }
     __syncwarp();
 
+    unsigned long long ph[kPhLaneSparse] = {};
+    long long tmark = clock64();
+    auto phase_end = [&](int k) {  // attribute cycles since the last mark to phase k
+        if (a.timing) {
+            const long long t = clock64();
+            ph[k] += t - tmark;
+            tmark = t;
+        }
+    };
     while (true) {
         uint32_t qi = 0;
         if (lane == 0) qi = atomicAdd(a.work, 1u);
@@ -669,6 +712,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
             }
         }
         if (ctx_used * 2 > a.ctxcap) err |= ERR_CTX;
+        phase_end(kPhSeeds);
 
         // ---- best-first expansion (search.cpp:218-264) ------------------
         uint32_t cursor = 0;
@@ -680,6 +724,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                 const uint32_t m = __ballot_sync(kFull, un);
                 if (m) upos = static_cast<int>(b + __ffs(m) - 1);
             }
+            phase_end(kPhSelect);
             if (upos < 0) break;
             cursor = upos;
             const uint32_t u = w.cand_n[upos] & kNodeMask;
@@ -726,6 +771,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                 }
             }
             __syncwarp();
+            phase_end(kPhAdj);
 
             // dedupe (reach order) + first-time detection
             uint32_t nnew = 0, nkeep = 0;
@@ -739,6 +785,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                 }
                 bool fresh = false;
                 if (keep) fresh = !bit_test_set(visited, x);
+                // first-time neighbours: pull their whole rows toward L2 now,
+                // one bulk prefetch per span, so the scoring chains below
+                // stream from L2 instead of paying a DRAM trip per stage
+                if (fresh && a.prefetch) prefetch_sparse(c, sq, x);
                 __syncwarp();
                 const uint32_t km = __ballot_sync(kFull, keep);
                 const uint32_t kpos = nkeep + __popc(km & ((1u << lane) - 1));
@@ -755,6 +805,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
             }
             nbc = nkeep;
             scored += nnew;
+            phase_end(kPhDedupe);
 
             // score first-time neighbours, lane per node.  Plain queries screen
             // against the worst entries of BOTH pools when both are full (an
@@ -766,6 +817,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
             score_staged(a, sq, w, lane, phase, nnew, [&](uint32_t i) { return w.nb[w.nnew[i]]; },
                          [&](uint32_t i, double d) { w.nd[w.nnew[i]] = d; }, qnorm, floor);
             __syncwarp();
+            phase_end(kPhScore);
 
             if (!ctx_mode) {
                 // cand: one sorted batch per 32 new nodes (order independent)
@@ -846,6 +898,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
                 }
                 cursor = 0;
             }
+            phase_end(kPhMerge);
         }
 
         // ---- keyword_postfilter (search.cpp:100-139) ---------------------
@@ -935,9 +988,68 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
             for (uint32_t i = lane; i < a.ctxcap; i += 32) ctx[i] = make_uint4(kEmpty, 0, 0, 0);
         }
         __syncwarp();
+        phase_end(kPhFinal);
+        if (a.timing && lane == 0) {
+            for (int k = 0; k < kPhLaneSparse; ++k) atomicAdd(&a.timing[k], ph[k]);
+            atomicAdd(&a.timing[kPhQueries], 1ull);
+            atomicAdd(&a.timing[kPhExpanded], expanded);
+            for (int k = 0; k < kPhLaneSparse; ++k) ph[k] = 0;
+        }
     }
 }
 
+}  // namespace
+}  // namespace fgb
+
+
+namespace fgb {
+namespace {
+constexpr uint64_t kId30 = 0x3FFFFFFFull;  // node ids must fit 30 bits in the plain kernel's pools
+
+// Device results -> the caller's fg_search_results (ids -> doc ids, per-query
+// validation errors, counters); records the kernel time of ev0..ev1.
+void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg_search_results* out,
+                    const std::vector<std::string>& errs, uint64_t nq, uint32_t stride,
+                    const DevBuf<uint32_t>& r_node, const DevBuf<double>& r_score,
+                    const DevBuf<uint32_t>& r_count, const DevBuf<uint32_t>& r_warn,
+                    const DevBuf<uint32_t>& r_err, const DevBuf<unsigned long long>& r_exp,
+                    const DevBuf<unsigned long long>& r_sc, cudaStream_t s) {
+    (void)q;
+    std::vector<uint32_t> h_node(nq * stride), h_count(nq), h_warn(nq), h_err(nq);
+    std::vector<double> h_score(nq * stride);
+    std::vector<unsigned long long> h_exp(nq), h_sc(nq);
+    r_node.download(h_node.data(), nq * stride, s);
+    r_score.download(h_score.data(), nq * stride, s);
+    r_count.download(h_count.data(), nq, s);
+    r_warn.download(h_warn.data(), nq, s);
+    r_err.download(h_err.data(), nq, s);
+    r_exp.download(h_exp.data(), nq, s);
+    r_sc.download(h_sc.data(), nq, s);
+    FGB_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
+    ix->last_kernel_ms = ms;
+    for (uint64_t i = 0; i < nq; ++i) {
+        if (h_err[i])
+            throw Error("internal", "search scratch overflow (twin/context table) on query " + std::to_string(i));
+        const uint32_t cnt = errs[i].empty() ? h_count[i] : 0;
+        out->hit_count[i] = cnt;
+        for (uint32_t j = 0; j < cnt; ++j) {
+            const uint32_t node = h_node[i * stride + j];
+            out->node[i * out->hit_stride + j] = node;
+            out->doc_id[i * out->hit_stride + j] = c.doc_id[node];
+            out->score[i * out->hit_stride + j] = h_score[i * stride + j];
+        }
+        if (out->expanded) out->expanded[i] = errs[i].empty() ? h_exp[i] : 0;
+        if (out->scored) out->scored[i] = errs[i].empty() ? h_sc[i] : 0;
+        if (out->warnings) out->warnings[i] = errs[i].empty() ? h_warn[i] : 0;
+        if (out->errors && out->error_stride) {
+            char* dst = out->errors + i * out->error_stride;
+            std::strncpy(dst, errs[i].c_str(), out->error_stride - 1);
+            dst[out->error_stride - 1] = 0;
+        }
+    }
+}
 }  // namespace
 }  // namespace fgb
 
@@ -1060,6 +1172,95 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         DevBuf<unsigned int> work(1);
         work.zero(s);
 
+        // ---- plain batches (no entity context, no required keywords): the
+        // certified-approximate kernel (search_plain.cu), bit-identical results
+        const char* pe = std::getenv("FGB_SEARCH_PLAIN");
+        const bool plain_ok = !any_ctx && !any_req && (!pe || pe[0] != '0') && n < kId30 && c.dc.meta;
+        if (plain_ok && nq) {
+            PlainLaunch pl{};
+            pl.c = c.dc;
+            pl.semantic = ix->semantic.get();
+            pl.degree = ix->degree;
+            pl.q = up.dq;
+            pl.norm_order = ix->norm_order.get();
+            pl.entry_count = norm_seeds;
+            pl.qflags = d_qflags.get();
+            pl.lcap = hash_capacity(up.max_lnnz);
+            pl.scap = hash_capacity(up.max_snnz);
+            pl.beamcap = std::max(max_beam, 32u);
+            pl.kcap = std::max(max_k, 1u);
+            pl.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
+            const double N = double(c.dstride) + c.max_lnnz + c.max_snnz + 2;
+            const double M = 4.0 * (((c.dstride >> 2) + 31) / 32) + 4.0 * ((std::max(c.max_lnnz, c.max_snnz) + 127) / 128) + 12;
+            pl.eps_coef = (N + M + 8) * std::ldexp(1.0, -53) * 1.01;
+            pl.eps_scale = 1.0;
+            if (const char* e = std::getenv("FGB_EPS_SCALE")) pl.eps_scale = std::atof(e);
+            pl.prefetch = 2;
+            if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) pl.prefetch = std::atoi(e);
+            if (plain_warp_smem(pl) > 0) {
+                const uint64_t slots = plain_slots(pl, nq, c.device);
+                pl.nwords = (n + 31) / 32;
+                pl.tcap = 65536;
+                if (ix->scratch_bits.size() < slots * pl.nwords) {
+                    ix->scratch_bits.alloc(slots * pl.nwords);
+                    ix->scratch_bits.zero(s);
+                }
+                pl.visited = ix->scratch_bits.get();
+                ix->scratch_lists.ensure(slots * pl.tcap);
+                pl.touched = ix->scratch_lists.get();
+                pl.hit_stride = stride;
+                pl.r_node = r_node.get();
+                pl.r_score = r_score.get();
+                pl.r_count = r_count.get();
+                pl.r_expanded = r_exp.get();
+                pl.r_scored = r_sc.get();
+                pl.r_warn = r_warn.get();
+                pl.r_err = r_err.get();
+                pl.work = work.get();
+                DevBuf<unsigned long long> timing, stats;
+                const char* te = std::getenv("FGB_SEARCH_TIMING");
+                if (te && te[0] == '1') {
+                    timing.alloc(kPlainPhCount);
+                    timing.zero(s);
+                    pl.timing = timing.get();
+                }
+                const char* se = std::getenv("FGB_SEARCH_STATS");
+                if ((se && se[0] == '1') || pl.eps_scale != 1.0) {
+                    stats.alloc(2);
+                    stats.zero(s);
+                    pl.stats = stats.get();
+                }
+                FGB_CUDA(cudaEventRecord(ix->ev0, s));
+                launch_search_plain(pl, nq, c.device, s);
+                FGB_CUDA(cudaEventRecord(ix->ev1, s));
+                if (pl.timing || pl.stats) {
+                    unsigned long long t[kPlainPhCount] = {}, st[2] = {};
+                    if (pl.timing) timing.download(t, kPlainPhCount, s);
+                    if (pl.stats) stats.download(st, 2, s);
+                    FGB_CUDA(cudaStreamSynchronize(s));
+                    float ms = 0;
+                    FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
+                    if (pl.timing) {
+                        const double X = t[kPlainPhExpanded] ? (double)t[kPlainPhExpanded] : 1.0;
+                        static const char* names[] = {"seeds", "select", "adjacency+visited", "sparse", "dense",
+                                                      "merge", "final"};
+                        std::fprintf(stderr, "[plain timing] %llu queries, %.1f expansions/query, %llu warps, %.3f ms\n",
+                                     t[kPlainPhQueries], X / std::max(1ull, t[kPlainPhQueries]),
+                                     (unsigned long long)slots, ms);
+                        for (int k = 0; k < kPlainPhQueries; ++k)
+                            std::fprintf(stderr, "  %-18s %10.0f cycles/expansion\n", names[k], t[k] / X);
+                    }
+                    if (pl.stats)
+                        std::fprintf(stderr, "[plain stats] exact resolutions %llu, exact final entries %llu\n",
+                                     st[0], st[1]);
+                }
+                finish_results(ix, c, q, out, errs, nq, stride, r_node, r_score, r_count, r_warn, r_err, r_exp,
+                               r_sc, s);
+                ix->last_launches = 1;
+                return;
+            }
+        }
+
         // ---- geometry
         SearchArgs a{};
         a.c = c.dc;
@@ -1162,46 +1363,37 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         a.r_err = r_err.get();
         a.work = work.get();
 
+        a.prefetch = 1;
+        if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) a.prefetch = std::atoi(e);
+        DevBuf<unsigned long long> timing;
+        const char* te = std::getenv("FGB_SEARCH_TIMING");
+        if (te && te[0] == '1') {
+            timing.alloc(kPhCount);
+            timing.zero(s);
+            a.timing = timing.get();
+        }
         FGB_CUDA(cudaEventRecord(ix->ev0, s));
         if (nq) search_kernel<<<(unsigned)blocks, kWarpsPerBlock * 32, block_smem, s>>>(a);
         FGB_LAUNCH("search_kernel");
         FGB_CUDA(cudaEventRecord(ix->ev1, s));
 
-        std::vector<uint32_t> h_node(nq * stride), h_count(nq), h_warn(nq), h_err(nq);
-        std::vector<double> h_score(nq * stride);
-        std::vector<unsigned long long> h_exp(nq), h_sc(nq);
-        r_node.download(h_node.data(), nq * stride, s);
-        r_score.download(h_score.data(), nq * stride, s);
-        r_count.download(h_count.data(), nq, s);
-        r_warn.download(h_warn.data(), nq, s);
-        r_err.download(h_err.data(), nq, s);
-        r_exp.download(h_exp.data(), nq, s);
-        r_sc.download(h_sc.data(), nq, s);
-        FGB_CUDA(cudaStreamSynchronize(s));
-        float ms = 0;
-        FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
-        ix->last_kernel_ms = ms;
+        finish_results(ix, c, q, out, errs, nq, stride, r_node, r_score, r_count, r_warn, r_err, r_exp, r_sc, s);
         ix->last_launches = nq ? 1 : 0;
-        for (uint64_t i = 0; i < nq; ++i) {
-            if (h_err[i])
-                throw Error("internal", "search scratch overflow (twin/context table) on query " +
-                                            std::to_string(i));
-            const uint32_t cnt = errs[i].empty() ? h_count[i] : 0;
-            out->hit_count[i] = cnt;
-            for (uint32_t j = 0; j < cnt; ++j) {
-                const uint32_t node = h_node[i * stride + j];
-                out->node[i * out->hit_stride + j] = node;
-                out->doc_id[i * out->hit_stride + j] = c.doc_id[node];
-                out->score[i * out->hit_stride + j] = h_score[i * stride + j];
-            }
-            if (out->expanded) out->expanded[i] = errs[i].empty() ? h_exp[i] : 0;
-            if (out->scored) out->scored[i] = errs[i].empty() ? h_sc[i] : 0;
-            if (out->warnings) out->warnings[i] = errs[i].empty() ? h_warn[i] : 0;
-            if (out->errors && out->error_stride) {
-                char* dst = out->errors + i * out->error_stride;
-                std::strncpy(dst, errs[i].c_str(), out->error_stride - 1);
-                dst[out->error_stride - 1] = 0;
-            }
+        if (a.timing) {
+            unsigned long long t[kPhCount];
+            timing.download(t, kPhCount, s);
+            FGB_CUDA(cudaStreamSynchronize(s));
+            const double X = t[kPhExpanded] ? (double)t[kPhExpanded] : 1.0;
+            static const char* names[] = {"seeds", "select", "adjacency", "dedupe+visited", "score",
+                                          "merge", "final"};
+            std::fprintf(stderr, "[search timing] %llu queries, %.1f expansions/query, %d warps, %.3f ms\n",
+                         t[kPhQueries], X / std::max(1ull, t[kPhQueries]), (int)slots, ix->last_kernel_ms);
+            for (int k = 0; k < kPhLaneSparse; ++k)
+                std::fprintf(stderr, "  %-15s %10.0f cycles/expansion\n", names[k], t[k] / X);
+            std::fprintf(stderr, "  lane: sparse %.0f cycles/node, dense %.0f cycles/node, scored %llu, dense rows %llu\n",
+                         t[kPhLaneSparse] / std::max(1.0, (double)t[kPhLaneScored]),
+                         t[kPhLaneDense] / std::max(1.0, (double)t[kPhLaneDenseRows]),
+                         t[kPhLaneScored], t[kPhLaneDenseRows]);
         }
     });
 }

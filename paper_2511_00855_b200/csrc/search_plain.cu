@@ -1,0 +1,727 @@
+// search_plain.cu — K5 for plain query batches (no entity context, no
+// required keywords): best-first beam search (search.cpp:141-280) with
+// CERTIFIED APPROXIMATE scoring and bit-identical results.
+//
+// Why.  The reference's hybrid score is a sequential fp64 sum (dense products
+// in index order, then each sparse path's shared-term products in ascending
+// order, scoring.cpp:10-99).  Reproducing those roundings needs one thread to
+// walk the whole 4 KB row serially: an uncoalesced, latency-bound stream
+// (tools/ubench_chain.cu: <= 2 elements/clk/SM from DRAM).  But a search only
+// needs the ORDER of distances, plus the exact values of the k results.
+//
+// How.  Each first-time neighbour is scored by the whole warp with coalesced
+// 16-byte loads: the same exact fp64 products (fp32 x fp32 is exact in fp64),
+// summed in a different order (per-lane partial sums + a butterfly).  Both
+// sums are within gamma_m * sum|p_i| of the exact real sum, and
+// sum|p_i| <= |q_w| * |d| <= |q_w| * sqrt(max sqnorm) (Cauchy-Schwarz over the
+// concatenated paths; sqnorm = the doc's unit-weight self score), so
+//     |approx - reference| <= eps = (N + M + 8) u |q_w| max|d|
+// (N, M = the two summation depths, u = 2^-53).  Every comparison the search
+// makes (batch sort, pool rank, eviction) is CERTIFIED when the two distances
+// differ by more than 2.5 eps; otherwise both entries are re-scored with the
+// reference's exact chain (hybrid_score, device_common.cuh) and compared
+// exactly (node id breaks ties, search.cpp:13-16).  So every decision equals
+// the reference's, the pools hold the same nodes in the same order, the
+// expansion sequence is identical, and the final top-k entries are re-scored
+// exactly: ids, order, scores, `expanded` and `scored` are bit-identical.
+//
+// Plain-query semantics used (search.cpp:22-42, 171-181): distances never
+// change after scoring, so a re-offer of a scored node is a no-op and the
+// pools' contents do not depend on offer order — each expansion's first-time
+// neighbours merge as one sorted batch; deleted nodes enter cand, never topk.
+#include <cstdio>
+
+#include "query_stage.cuh"
+#include "search_plain.hpp"
+
+namespace fgb {
+namespace {
+
+constexpr uint32_t kExp = 0x80000000u;    // cand entry expanded
+constexpr uint32_t kExact = 0x40000000u;  // stored distance is the reference's exact value
+constexpr uint32_t kId = 0x3FFFFFFFu;
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr int kSG = 8;         // sparse rows in flight per warp round trip
+constexpr int kMinWarps = 12;  // launch bound: query-warps per SM (register budget)
+enum : uint32_t { QF_VALID = 1, QF_ENTITY = 2, QF_FALLBACK = 4 };
+
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000ll); }
+
+__device__ __forceinline__ bool eless(double d1, uint32_t n1, double d2, uint32_t n2) {
+    return d1 < d2 || (d1 == d2 && n1 < n2);  // entry_less (search.cpp:13-16)
+}
+
+// The two stored distances decide their order exactly.
+__device__ __forceinline__ bool certain(double da, uint32_t na, double db, uint32_t nb, double tol) {
+    return ((na & nb & kExact) != 0) || fabs(da - db) > tol;
+}
+
+// The reference's exact distance — the sequential chains of
+// scoring.cpp:10-99 (dense in index order, then each sparse path's shared
+// terms in ascending order; products exact, one rounding per add).  The rare
+// path (uncertain comparisons, final top-k): few registers.  (Kept inline:
+// an out-of-line call here corrupted live batch registers under sm_100a
+// ptxas 12.9 — tools/smoke_plain.py reproduces it with __noinline__.)
+__device__ __forceinline__ double exact_dist(const DevCorpus* c, SmemQuery sq, uint32_t node) {
+    double acc = 0.0;
+    if (sq.dense) {
+        const float* row = c->dense + static_cast<uint64_t>(node) * c->dstride;
+        for (uint32_t i = 0; i < c->dstride; ++i) acc = __dadd_rn(acc, __dmul_rn(sq.dense[i], (double)row[i]));
+    }
+    for (int path = 0; path < 2; ++path) {
+        const bool learned = path == 0;
+        const uint32_t mask = learned ? sq.lmask : sq.smask;
+        double s = 0.0;
+        if (mask) {
+            const uint64_t off = learned ? c->l_off[node] : c->s_off[node];
+            const uint32_t nnz = learned ? c->l_nnz[node] : c->s_nnz[node];
+            const uint32_t* idx = (learned ? c->l_idx : c->s_idx) + off;
+            const float* val = (learned ? c->l_val : c->s_val) + off;
+            for (uint32_t j = 0; j < nnz; ++j)
+                probe_term(idx[j], val[j], learned ? sq.lkeys : sq.skeys, learned ? sq.lvals : sq.svals, mask,
+                           learned ? sq.lfilt : sq.sfilt, s);
+        }
+        acc = __dadd_rn(acc, s);
+    }
+    return -acc;
+}
+
+// ------------------------------------------------------------ scoring
+// Adds the products of the query terms among 4 postings; the filter tests
+// are branch-free, the hash is probed only for filter hits.
+__device__ __forceinline__ void probe4(const uint4& ii, const float4& vv, const uint32_t* keys, const float* vals,
+                                       const uint32_t* filt, uint32_t mask, double& s) {
+    const uint32_t fm = 2 * mask + 1;
+    const uint32_t t[4] = {ii.x, ii.y, ii.z, ii.w};
+    const float v[4] = {vv.x, vv.y, vv.z, vv.w};
+    uint32_t hits = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hits |= static_cast<uint32_t>(t[k] != kPad && filter_hit(filt, fm, t[k])) << k;
+    if (hits) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float q;
+            if (((hits >> k) & 1u) && hash_find(keys, vals, mask, t[k], q)) s = __fma_rn((double)q, (double)v[k], s);
+        }
+    }
+}
+
+// Reduce-scatter of kSG per-lane partial sums: node k's total (over all 32
+// lanes) ends in lanes [4k, 4k + 4) (bit-identical there).  9 shuffles
+// instead of 8 full butterflies.
+__device__ __forceinline__ double reduce_scatter8(double (&x)[8], uint32_t lane) {
+    const bool b4 = (lane >> 4) & 1u, b3 = (lane >> 3) & 1u, b2 = (lane >> 2) & 1u;
+    double y[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? x[i] : x[i + 4];
+        y[i] = (b4 ? x[i + 4] : x[i]) + __shfl_xor_sync(kFull, send, 16);
+    }
+    double z[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? y[i] : y[i + 2];
+        z[i] = (b3 ? y[i + 2] : y[i]) + __shfl_xor_sync(kFull, send, 8);
+    }
+    double r = (b2 ? z[1] : z[0]) + __shfl_xor_sync(kFull, b2 ? z[0] : z[1], 4);
+    r += __shfl_xor_sync(kFull, r, 2);
+    r += __shfl_xor_sync(kFull, r, 1);
+    return r;
+}
+
+// Warp-cooperative approximate sparse dot of one path for the F nodes held
+// by lanes 0..F-1 ((off4, nnz) each); lane j receives node j's sum.  kSG
+// nodes' first 128 postings (idx + val, coalesced 512 B each) are in flight
+// per round trip; longer rows load the rest synchronously.
+__device__ __forceinline__ double sparse_group(const uint32_t* idx, const float* val, const uint32_t* keys,
+                                               const float* vals, const uint32_t* filt, uint32_t mask,
+                                               uint32_t off4, uint32_t nnz, uint32_t lane, uint32_t F) {
+    double mine = 0.0;
+    const uint4* i4 = reinterpret_cast<const uint4*>(idx);
+    const float4* v4 = reinterpret_cast<const float4*>(val);
+#pragma unroll 1
+    for (uint32_t g = 0; g < F; g += kSG) {
+        uint4 ii[kSG];
+        float4 vv[kSG];
+#pragma unroll
+        for (int k = 0; k < kSG; ++k) {
+            const uint32_t j = g + k;
+            const uint32_t oj = __shfl_sync(kFull, off4, j & 31);
+            const uint32_t nj = __shfl_sync(kFull, nnz, j & 31);
+            if (j < F && 4 * lane < nj) {
+                ii[k] = __ldg(i4 + oj + lane);
+                vv[k] = __ldg(v4 + oj + lane);
+            } else {
+                ii[k] = make_uint4(kPad, kPad, kPad, kPad);
+                vv[k] = make_float4(0, 0, 0, 0);
+            }
+        }
+        double part[8];
+#pragma unroll
+        for (int k = 0; k < kSG; ++k) {
+            part[k] = 0.0;
+            probe4(ii[k], vv[k], keys, vals, filt, mask, part[k]);
+        }
+        // postings 128.. of long rows (not taken for nnz <= 128)
+#pragma unroll
+        for (int k = 0; k < kSG; ++k) {
+            const uint32_t j = g + k;
+            const uint32_t oj = __shfl_sync(kFull, off4, j & 31);
+            const uint32_t nj_all = __shfl_sync(kFull, nnz, j & 31);
+            const uint32_t nj = j < F ? nj_all : 0u;
+            for (uint32_t base = 32; 4 * base < nj; base += 32)
+                if (4 * (base + lane) < nj)
+                    probe4(__ldg(i4 + oj + base + lane), __ldg(v4 + oj + base + lane), keys, vals, filt, mask,
+                           part[k]);
+        }
+        const double r = reduce_scatter8(part, lane);
+        const uint32_t k = lane - g;  // owner lane g + k takes node k's sum from lane 4k
+        const double got = __shfl_sync(kFull, r, (4 * k) & 31);
+        if (lane >= g && lane < g + kSG) mine = got;
+    }
+    return mine;
+}
+
+template <int NQ4>
+__device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, uint32_t lane, float4 (&b)[NQ4]) {
+    const float4* row = reinterpret_cast<const float4*>(c.dense + static_cast<uint64_t>(node) * c.dstride);
+    const uint32_t n4 = c.dstride >> 2;
+#pragma unroll
+    for (int k = 0; k < NQ4; ++k) {
+        const uint32_t col = k * 32 + lane;
+        b[k] = col < n4 ? __ldg(row + col) : make_float4(0, 0, 0, 0);
+    }
+}
+
+// Warp-cooperative approximate dense dot (coalesced 512-B loads per warp
+// instruction) for every lane-held node in `mask`, two rows per round trip.
+template <int NQ4>
+__device__ __forceinline__ double dense_group(const DevCorpus& c, const double* q, uint32_t node, uint32_t lane,
+                                              uint32_t mask) {
+    double mine = 0.0;
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    const uint32_t n4 = c.dstride >> 2;
+    uint32_t m = mask;
+#pragma unroll 1
+    while (m) {
+        const uint32_t j0 = __ffs(m) - 1;
+        m &= m - 1;
+        const bool two = m != 0;
+        const uint32_t j1 = two ? __ffs(m) - 1 : j0;
+        if (two) m &= m - 1;
+        const uint32_t n0 = __shfl_sync(kFull, node, j0), n1 = __shfl_sync(kFull, node, j1);
+        float4 ra[NQ4], rb[NQ4];
+        dense_load<NQ4>(c, n0, lane, ra);
+        dense_load<NQ4>(c, n1, lane, rb);  // (j1 == j0 when alone: an L1 hit, result unused)
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int k = 0; k < NQ4; ++k) {
+            const uint32_t col = k * 32 + lane;
+            if (col < n4) {
+                const double2 x = q2[2 * col], y = q2[2 * col + 1];
+                sa = __fma_rn(x.x, (double)ra[k].x, sa);
+                sa = __fma_rn(x.y, (double)ra[k].y, sa);
+                sa = __fma_rn(y.x, (double)ra[k].z, sa);
+                sa = __fma_rn(y.y, (double)ra[k].w, sa);
+                sb = __fma_rn(x.x, (double)rb[k].x, sb);
+                sb = __fma_rn(x.y, (double)rb[k].y, sb);
+                sb = __fma_rn(y.x, (double)rb[k].z, sb);
+                sb = __fma_rn(y.y, (double)rb[k].w, sb);
+            }
+        }
+        // reduce-scatter of the pair: lanes 0-15 end with a's sum, 16-31 with b's
+        const bool hi = lane >= 16;
+        double r = (hi ? sb : sa) + __shfl_xor_sync(kFull, hi ? sa : sb, 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+        const double ga = __shfl_sync(kFull, r, 0), gb = __shfl_sync(kFull, r, 16);
+        if (lane == j0) mine = ga;
+        if (two && lane == j1) mine = gb;
+    }
+    return mine;
+}
+
+// ------------------------------------------------------------ pools
+struct Pool {
+    double* d;
+    uint32_t* n;  // node | kExact (| kExp for cand)
+    uint32_t cap;
+};
+
+// # entries strictly before (d, node) by the stored keys.
+__device__ __forceinline__ uint32_t pool_rank(const Pool& p, uint32_t size, double d, uint32_t node) {
+    uint32_t lo = 0, hi = size;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (eless(p.d[mid], p.n[mid] & kId, d, node))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Bitonic sort of one (d, n) per lane by (d, node); invalid lanes carry
+// (+inf, kEmpty) and sort last.
+__device__ __forceinline__ void warp_sort(double& d, uint32_t& n, uint32_t lane) {
+#pragma unroll
+    for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            const double od = __shfl_xor_sync(kFull, d, j);
+            const uint32_t on = __shfl_xor_sync(kFull, n, j);
+            const bool up = (lane & k) == 0;
+            const bool lower = (lane & j) == 0;
+            const bool other_less = eless(od, on & kId, d, n & kId);
+            const bool take = (lower == up) ? other_less : (!other_less && (od != d || on != n));
+            if (take) {
+                d = od;
+                n = on;
+            }
+        }
+    }
+}
+
+// Inserts m <= 32 new entries (sorted, lanes < m, ranks certified exact and
+// non-decreasing) into the pool: the set result of offering them one by one
+// (Pool::offer, search.cpp:26-42).  Returns the smallest insertion position.
+__device__ __forceinline__ uint32_t pool_insert(const Pool& p, uint32_t& size, double d, uint32_t n, uint32_t m,
+                                                uint32_t rank, uint32_t lane, uint32_t* br) {
+    const uint32_t mypos = lane < m ? lane + rank : p.cap;
+    uint32_t p0 = mypos;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p0 = min(p0, __shfl_xor_sync(kFull, p0, o));
+    if (p0 >= p.cap) return p.cap;
+    __syncwarp();
+    if (lane < m) br[lane] = rank;
+    __syncwarp();
+    // pool entry i >= p0 moves right by #{j : rank_j <= i}; right to left,
+    // each lane's count only shrinks (i decreases by 32 per step)
+    int b = static_cast<int>(((size - 1) / 32) * 32);
+    uint32_t sh = m;
+    {
+        const uint32_t i = b + lane;
+        while (sh > 0 && br[sh - 1] > i) --sh;
+    }
+#pragma unroll 1
+    for (; size > p0 && b >= static_cast<int>(p0 & ~31u); b -= 32) {
+        const uint32_t i = b + lane;
+        while (sh > 0 && br[sh - 1] > i) --sh;
+        const bool v = i < size && i >= p0;
+        double dd = 0;
+        uint32_t nn = 0;
+        if (v) {
+            dd = p.d[i];
+            nn = p.n[i];
+        }
+        __syncwarp();
+        if (v && i + sh < p.cap) {
+            p.d[i + sh] = dd;
+            p.n[i + sh] = nn;
+        }
+        __syncwarp();
+    }
+    if (lane < m && mypos < p.cap) {
+        p.d[mypos] = d;
+        p.n[mypos] = n;  // new entries are unexpanded
+    }
+    __syncwarp();
+    size = min(size + m, p.cap);
+    return p0;
+}
+
+struct PlainMem {
+    unsigned char* stage;
+    double* cand_d;
+    uint32_t* cand_n;
+    double* topk_d;
+    uint32_t* topk_n;
+    uint32_t* br;
+};
+
+__device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+__device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch& a) {
+    PlainMem m;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = base + off;
+        off += al16(bytes);
+        return p;
+    };
+    m.stage = take(stage_bytes(a.c.dstride, a.lcap, a.scap));
+    m.cand_d = reinterpret_cast<double*>(take(a.beamcap * 8));
+    m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
+    m.cand_n = reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
+    m.topk_n = reinterpret_cast<uint32_t*>(take(a.kcap * 4));
+    m.br = reinterpret_cast<uint32_t*>(take(32 * 4));
+    return m;
+}
+
+template <int NQ4, bool kTime>
+__global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ DevCorpus cs;  // for the out-of-line exact scorer
+    const uint32_t lane = threadIdx.x & 31;
+    if (lane == 0) cs = a.c;
+    __syncwarp();
+    const uint64_t slot = blockIdx.x;
+    PlainMem w = carve(smem_raw, a);
+    uint32_t* visited = a.visited + slot * a.nwords;
+    uint32_t* touched = a.touched + slot * a.tcap;
+    const DevCorpus& c = a.c;
+    unsigned long long ph[kTime ? kPlainPhQueries : 1] = {};
+    long long tmark = kTime ? clock64() : 0;
+    auto phase_end = [&](int k) {
+        if constexpr (kTime) {
+            const long long t = clock64();
+            ph[k] += t - tmark;
+            tmark = t;
+        }
+    };
+    unsigned long long resolved = 0, final_exact = 0;
+
+#pragma unroll 1
+    while (true) {
+        uint32_t qi = 0;
+        if (lane == 0) qi = atomicAdd(a.work, 1u);
+        qi = __shfl_sync(kFull, qi, 0);
+        if (qi >= a.q.count) break;
+        const uint32_t flags = a.qflags[qi];
+        if (!(flags & QF_VALID)) {
+            if (lane == 0) {
+                a.r_count[qi] = 0;
+                a.r_expanded[qi] = 0;
+                a.r_scored[qi] = 0;
+                a.r_warn[qi] = 0;
+                a.r_err[qi] = 0;
+            }
+            continue;
+        }
+        const uint32_t K = a.q.k[qi], B = a.q.beam[qi];
+        SmemQuery sq;
+        stage_query(a.q, qi, c.dstride, w.stage, a.lcap, a.scap, lane, 32, sq, [] { __syncwarp(); });
+        // |weighted dense query| (screening) and |weighted query| over all paths (error bound)
+        double qd2 = 0.0, qs2 = 0.0;
+        if (sq.dense)
+            for (uint32_t j = lane; j < c.dstride; j += 32) qd2 += sq.dense[j] * sq.dense[j];
+        for (uint32_t j = lane; j < a.lcap; j += 32)
+            if (sq.lmask && sq.lkeys[j] != kEmpty) qs2 += (double)sq.lvals[j] * (double)sq.lvals[j];
+        for (uint32_t j = lane; j < a.scap; j += 32)
+            if (sq.smask && sq.skeys[j] != kEmpty) qs2 += (double)sq.svals[j] * (double)sq.svals[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            qd2 += __shfl_xor_sync(kFull, qd2, o);
+            qs2 += __shfl_xor_sync(kFull, qs2, o);
+        }
+        const double qnorm = sqrt(qd2) * (1.0 + 1e-12);
+        const double eps = a.eps_coef * (sqrt(qd2 + qs2) * (1.0 + 1e-10)) * a.max_norm * a.eps_scale + 1e-300;
+        const double tol = 2.5 * eps;
+
+        const Pool topk{w.topk_d, w.topk_n, K};
+        const Pool cand{w.cand_d, w.cand_n, B};
+        uint32_t tsize = 0, csize = 0, ntouched = 0, cursor = 0;
+        uint32_t seed_next = 0, adj_u = 0, adj_b = a.degree;
+        unsigned long long expanded = 0, scored = 0;
+
+#pragma unroll 1
+        while (true) {
+            // ---- the next lane-held batch: the entry_count largest-norm seeds
+            // (search.cpp:205-216), then the neighbours of the first
+            // unexpanded cand entry, 32 at a time (search.cpp:218-264)
+            uint32_t node = 0;
+            bool v = false;
+            if (seed_next < a.entry_count) {
+                const uint32_t i = seed_next + lane;
+                v = i < a.entry_count;
+                if (v) node = a.norm_order[i];
+                seed_next += 32;
+            } else {
+                if (adj_b >= a.degree) {
+                    phase_end(kPlainPhSeeds);
+                    int upos = -1;
+                    for (uint32_t b = cursor; b < csize && upos < 0; b += 32) {
+                        const uint32_t i = b + lane;
+                        const uint32_t m = __ballot_sync(kFull, i < csize && !(w.cand_n[i] & kExp));
+                        if (m) upos = static_cast<int>(b + __ffs(m) - 1);
+                    }
+                    phase_end(kPlainPhSelect);
+                    if (upos < 0) break;
+                    cursor = upos;
+                    __syncwarp();
+                    adj_u = w.cand_n[upos] & kId;
+                    __syncwarp();
+                    if (lane == 0) w.cand_n[upos] |= kExp;
+                    __syncwarp();
+                    ++expanded;
+                    adj_b = 0;
+                }
+                const uint32_t j = adj_b + lane;
+                v = j < a.degree;
+                if (v) node = a.semantic[static_cast<uint64_t>(adj_u) * a.degree + j];
+                adj_b += 32;
+            }
+            // first-time test (a repeated neighbour loses the test-and-set to
+            // its first copy, so no explicit dedupe is needed)
+            bool fresh = false;
+            if (v) {
+                const uint32_t bit = 1u << (node & 31);
+                fresh = (atomicOr(&visited[node >> 5], bit) & bit) == 0;
+            }
+            const uint32_t fm = __ballot_sync(kFull, fresh);
+            phase_end(kPlainPhAdj);
+            if (!fm) continue;
+
+            // ---- score the F fresh nodes, compacted into lanes 0..F-1
+            const uint32_t F = __popc(fm);
+            const uint32_t src = __fns(fm, 0, lane + 1);
+            const uint32_t cn = __shfl_sync(kFull, node, src < 32 ? src : 0);
+            const bool mine = lane < F;
+            if (mine && ntouched + lane < a.tcap) touched[ntouched + lane] = cn;
+            ntouched += F;
+            scored += F;
+            uint4 mt = make_uint4(0, 0, 0, 0);  // one 16-B record: sparse offsets/lengths, dense norm
+            if (mine) {
+                mt = __ldg(c.meta + cn);
+                if (sq.dense && a.prefetch >= 2)
+                    l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
+            }
+            double L = 0.0, S = 0.0;
+#pragma unroll 1
+            for (int path = 0; path < 2; ++path) {
+                const bool learned = path == 0;
+                const uint32_t pm = learned ? sq.lmask : sq.smask;
+                if (!pm) continue;
+                const double r = sparse_group(learned ? c.l_idx : c.s_idx, learned ? c.l_val : c.s_val,
+                                              learned ? sq.lkeys : sq.skeys, learned ? sq.lvals : sq.svals,
+                                              learned ? sq.lfilt : sq.sfilt, pm, learned ? mt.x : mt.y,
+                                              learned ? (mt.z & 0xFFFFu) : (mt.z >> 16), lane, F);
+                if (learned)
+                    L = r;
+                else
+                    S = r;
+            }
+            phase_end(kPlainPhSparse);
+            // screening against both full pools' worst entries (an offer
+            // below both is a no-op); bounds widened by the error terms
+            bool keep = mine;
+            if (mine && csize == B && tsize == K) {
+                const double floor = fmin(-w.cand_d[csize - 1], -w.topk_d[tsize - 1]) - 4.0 * eps;
+                const double dn = sq.dense ? (double)__uint_as_float(mt.w) : 0.0;
+                const double ub = score_upper_bound(sq.dense ? qnorm : 0.0, dn, L, S) + 2.0 * eps;
+                keep = !(ub < floor);
+            }
+            const uint32_t km = __ballot_sync(kFull, keep);
+            if (keep && sq.dense && a.prefetch == 1)
+                l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
+            const double D = sq.dense ? dense_group<NQ4>(c, sq.dense, cn, lane, km) : 0.0;
+            phase_end(kPlainPhDense);
+            const uint32_t m = __popc(km);
+            if (m == 0) continue;
+            double d = keep ? -__dadd_rn(__dadd_rn(D, L), S) : dinf();
+            uint32_t n = keep ? cn : kEmpty;
+
+            // ---- certify: sort the batch, then every adjacent pair and every
+            // new entry's neighbours at its rank in both pools must be
+            // decided by the stored distances; otherwise re-score exactly
+            uint32_t rank_t = 0, rank_c = 0, tm = 0;
+            double td = dinf();
+            uint32_t tn = kEmpty;
+#pragma unroll 1
+            while (true) {
+                warp_sort(d, n, lane);
+                const double dn2 = __shfl_down_sync(kFull, d, 1);
+                const uint32_t nn2 = __shfl_down_sync(kFull, n, 1);
+                const bool bad = lane < 31 && n != kEmpty && nn2 != kEmpty && !certain(d, n, dn2, nn2, tol);
+                // (every shuffle runs on all 32 lanes: never inside a short-circuit)
+                const bool prev_bad = __shfl_up_sync(kFull, bad, 1);
+                bool fix = (bad || (prev_bad && lane > 0)) && n != kEmpty && !(n & kExact);
+#ifdef FGB_DEBUG_PLAIN
+                if (lane < m && n == kEmpty)
+                    printf("BAD lane %u m %u F %u km %08x d %g L %g S %g D %g keep %d cn %u\n", lane, m, F, km, d, L, S, D,
+                           (int)keep, cn);
+                if (lane < m && (n & kId) >= c.n)
+                    printf("BADID lane %u m %u F %u km %08x d %g n %08x keep %d cn %u\n", lane, m, F, km, d, n,
+                           (int)keep, cn);
+#endif
+                // topk view: the non-deleted entries, in order (search.cpp:174)
+                const bool ok = lane < m && !c.deleted[n & kId];
+                const uint32_t om = __ballot_sync(kFull, ok);
+                const uint32_t ts = __fns(om, 0, lane + 1);
+                tm = __popc(om);
+                td = __shfl_sync(kFull, d, ts < 32 ? ts : 0);
+                tn = __shfl_sync(kFull, n, ts < 32 ? ts : 0);
+                if (lane >= tm) {
+                    td = dinf();
+                    tn = kEmpty;
+                }
+                bool need_t = false, need_c = false;
+                if (!__any_sync(kFull, fix)) {
+                    if (lane < tm) {
+                        rank_t = pool_rank(topk, tsize, td, tn & kId);
+                        need_t = (rank_t > 0 && !certain(w.topk_d[rank_t - 1], w.topk_n[rank_t - 1], td, tn, tol)) ||
+                                 (rank_t < tsize && !certain(td, tn, w.topk_d[rank_t], w.topk_n[rank_t], tol));
+                    }
+                    if (lane < m) {
+                        rank_c = pool_rank(cand, csize, d, n & kId);
+                        need_c = (rank_c > 0 && !certain(w.cand_d[rank_c - 1], w.cand_n[rank_c - 1], d, n, tol)) ||
+                                 (rank_c < csize && !certain(d, n, w.cand_d[rank_c], w.cand_n[rank_c], tol));
+                    }
+                    // a topk view entry in doubt marks its batch lane
+                    const uint32_t myview = __popc(om & ((1u << lane) - 1));
+                    const bool view_doubt = __shfl_sync(kFull, need_t, myview & 31);
+                    fix = need_c || (ok && view_doubt);
+                    fix = fix && !(n & kExact);
+                }
+                const uint32_t ntm = __ballot_sync(kFull, need_t), ncm = __ballot_sync(kFull, need_c);
+                const uint32_t fxm = __ballot_sync(kFull, fix);
+                if (!fxm && !ntm && !ncm) break;
+                if (fix) {
+                    d = exact_dist(&cs, sq, n & kId);
+                    n |= kExact;
+                }
+                resolved += __popc(fxm);
+                // pool entries around the doubtful ranks get exact distances too
+#pragma unroll 1
+                for (int pi = 0; pi < 2; ++pi) {
+                    const Pool& P = pi ? cand : topk;
+                    const uint32_t sz = pi ? csize : tsize;
+                    uint32_t nm = pi ? ncm : ntm;
+                    const uint32_t rk = pi ? rank_c : rank_t;
+                    while (nm) {
+                        const uint32_t j = __ffs(nm) - 1;
+                        nm &= nm - 1;
+                        const int i = static_cast<int>(__shfl_sync(kFull, rk, j)) - 4 + static_cast<int>(lane);
+                        const bool pf = lane < 8 && i >= 0 && i < static_cast<int>(sz) && !(P.n[i] & kExact);
+                        if (pf) {
+                            P.d[i] = exact_dist(&cs, sq, P.n[i] & kId);
+                            P.n[i] |= kExact;
+                        }
+                        resolved += __popc(__ballot_sync(kFull, pf));
+                        __syncwarp();
+                    }
+                }
+            }
+            pool_insert(topk, tsize, td, tn, tm, rank_t, lane, w.br);
+            const uint32_t p0 = pool_insert(cand, csize, d, n, m, rank_c, lane, w.br);
+            cursor = min(cursor, p0);
+            phase_end(kPlainPhMerge);
+        }
+
+        // ---- results: the top-k with the reference's exact scores
+        // (keyword_postfilter with no required keywords: topk as is, search.cpp:100-139)
+        for (uint32_t i = lane; i < tsize; i += 32) {
+            if (!(w.topk_n[i] & kExact)) {
+                w.topk_d[i] = exact_dist(&cs, sq, w.topk_n[i] & kId);
+                ++final_exact;
+            }
+            a.r_node[static_cast<uint64_t>(qi) * a.hit_stride + i] = w.topk_n[i] & kId;
+            a.r_score[static_cast<uint64_t>(qi) * a.hit_stride + i] = -w.topk_d[i];
+        }
+        if (lane == 0) {
+            a.r_count[qi] = tsize;
+            a.r_expanded[qi] = expanded;
+            a.r_scored[qi] = scored;
+            a.r_warn[qi] = (flags & QF_FALLBACK) ? 1u : 0u;
+            a.r_err[qi] = 0;
+        }
+        // ---- reset the visited bits
+        if (ntouched <= a.tcap) {
+            for (uint32_t i = lane; i < ntouched; i += 32) visited[touched[i] >> 5] = 0;
+        } else {
+            for (uint64_t i = lane; i < a.nwords; i += 32) visited[i] = 0;
+        }
+        __syncwarp();
+        phase_end(kPlainPhFinal);
+        if (kTime && lane == 0) {
+            for (int k = 0; k < kPlainPhQueries; ++k) {
+                atomicAdd(&a.timing[k], ph[k]);
+                ph[k] = 0;
+            }
+            atomicAdd(&a.timing[kPlainPhQueries], 1ull);
+            atomicAdd(&a.timing[kPlainPhExpanded], expanded);
+        }
+    }
+    if (a.stats) {
+        const unsigned long long fe = __reduce_add_sync(kFull, static_cast<unsigned>(final_exact));
+        if (lane == 0) {
+            atomicAdd(&a.stats[0], resolved);
+            atomicAdd(&a.stats[1], fe);
+        }
+    }
+}
+
+template <int NQ4>
+void launch_t(const PlainLaunch& a, uint64_t blocks, size_t smem, cudaStream_t s) {
+    if (a.timing) {
+        FGB_CUDA(cudaFuncSetAttribute(search_plain_kernel<NQ4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        search_plain_kernel<NQ4, true><<<(unsigned)blocks, 32, smem, s>>>(a);
+    } else {
+        FGB_CUDA(cudaFuncSetAttribute(search_plain_kernel<NQ4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        search_plain_kernel<NQ4, false><<<(unsigned)blocks, 32, smem, s>>>(a);
+    }
+    FGB_LAUNCH("search_plain_kernel");
+}
+
+int nq4_of(const PlainLaunch& a) {
+    const uint32_t need = ((a.c.dstride >> 2) + 31) / 32;
+    for (int v : {1, 2, 3, 4, 6, 8})
+        if (static_cast<uint32_t>(v) >= need) return v;
+    return 0;
+}
+
+template <int NQ4>
+const void* kernel_ptr() {
+    return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false>);
+}
+
+const void* kernel_for(int v) {
+    switch (v) {
+        case 1: return kernel_ptr<1>();
+        case 2: return kernel_ptr<2>();
+        case 3: return kernel_ptr<3>();
+        case 4: return kernel_ptr<4>();
+        case 6: return kernel_ptr<6>();
+        case 8: return kernel_ptr<8>();
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+size_t plain_warp_smem(const PlainLaunch& a) {
+    if (nq4_of(a) == 0) return 0;  // dense rows wider than 1,024 floats: general kernel
+    auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
+    const size_t b = al(stage_bytes(a.c.dstride, a.lcap, a.scap)) + al(a.beamcap * 8) + al(a.kcap * 8) +
+                     al(a.beamcap * 4) + al(a.kcap * 4) + al(32 * 4);
+    return b <= 227 * 1024 ? b : 0;
+}
+
+uint64_t plain_slots(const PlainLaunch& a, uint64_t nq, int device) {
+    const size_t smem = plain_warp_smem(a);
+    const void* k = kernel_for(nq4_of(a));
+    FGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, sms = 0;
+    FGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem));
+    FGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    per_sm = std::max(per_sm, 1);
+    return std::max<uint64_t>(1, std::min<uint64_t>(nq, static_cast<uint64_t>(sms) * per_sm));
+}
+
+void launch_search_plain(const PlainLaunch& a, uint64_t nq, int device, cudaStream_t s) {
+    const size_t smem = plain_warp_smem(a);
+    const uint64_t blocks = plain_slots(a, nq, device);
+    switch (nq4_of(a)) {
+        case 1: launch_t<1>(a, blocks, smem, s); break;
+        case 2: launch_t<2>(a, blocks, smem, s); break;
+        case 3: launch_t<3>(a, blocks, smem, s); break;
+        case 4: launch_t<4>(a, blocks, smem, s); break;
+        case 6: launch_t<6>(a, blocks, smem, s); break;
+        case 8: launch_t<8>(a, blocks, smem, s); break;
+        default: throw Error("internal", "plain search: unsupported dense width");
+    }
+}
+
+}  // namespace fgb

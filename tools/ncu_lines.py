@@ -1,6 +1,6 @@
 """Aggregate ncu warp-stall samples per CUDA source line.
 
-  python tools/ncu_lines.py <report.ncu-rep> <object.o> <kernel-substring> [top]
+  python tools/ncu_lines.py <report.ncu-rep> <object.o> <ncu-kernel-regex> [top] [sass-function-substring]
 
 Exports the report's SASS source page, disassembles the kernel's cubin from
 the object with line info (nvdisasm --print-line-info), maps every sampled
@@ -19,6 +19,7 @@ import tempfile
 def main():
     rep, obj, kname = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+    fname = sys.argv[5] if len(sys.argv) > 5 else kname
     page = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kname}"],
                           capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(page)))
@@ -37,7 +38,7 @@ def main():
     line_of = {}
     for ln in dis.splitlines():
         if ln.startswith("//----") or ln.startswith("\t.section"):
-            infn = kname in ln
+            infn = fname in ln
             continue
         if not infn:
             continue

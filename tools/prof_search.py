@@ -15,6 +15,7 @@ ap.add_argument("--docs", type=int, default=100000)
 ap.add_argument("--queries", type=int, default=2000)
 ap.add_argument("--beam", type=int, default=256)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--entry", type=int, default=32)
 a = ap.parse_args()
 p = A.synth_params(docs=a.docs, dense_dim=768, learned_vocab=30522, learned_nnz=120,
                    statistical_vocab=0, statistical_nnz=40, seed=1)
@@ -34,7 +35,7 @@ else:
 q = synth.synth_queries(p, a.queries).with_(beam_width=a.beam)
 for _ in range(a.reps):
     t = time.time()
-    r = fg.batch_query(ix, q)
+    r = fg.batch_query(ix, q, entry_count=a.entry)
     ms, _ = ix.last_search_stats()
     print(f"beam {a.beam}: {q.count / (ms / 1e3):.0f} QPS kernel, scored {r.scored.mean():.0f}, "
           f"expanded {r.expanded.mean():.0f}, wall {time.time() - t:.3f}s", flush=True)
