@@ -219,6 +219,9 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             std::vector<float> val;
             build_sparse(v->learned, n, off, nnz, idx, val, c->max_lnnz, "learned");
             c->l_nnz_total4 = idx.size() / 4;
+            c->l_vocab = 0;
+            for (uint32_t t : idx)
+                if (t != kPad) c->l_vocab = std::max(c->l_vocab, t + 1);
             c->l_off.upload(off, s);
             c->l_nnz.upload(nnz, s);
             c->l_idx.upload(idx.empty() ? std::vector<uint32_t>(4, kPad) : idx, s);
@@ -226,6 +229,9 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             FGB_CUDA(cudaStreamSynchronize(s));
             build_sparse(v->statistical, n, off, nnz, idx, val, c->max_snnz, "statistical");
             c->s_nnz_total4 = idx.size() / 4;
+            c->s_vocab = 0;
+            for (uint32_t t : idx)
+                if (t != kPad) c->s_vocab = std::max(c->s_vocab, t + 1);
             c->s_off.upload(off, s);
             c->s_nnz.upload(nnz, s);
             c->s_idx.upload(idx.empty() ? std::vector<uint32_t>(4, kPad) : idx, s);
@@ -294,6 +300,13 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
         FGB_CUDA(cudaStreamSynchronize(s));
         c->max_sqnorm = 0.0;
         for (double x : c->sqnorm_h) c->max_sqnorm = std::max(c->max_sqnorm, x);
+        {
+            std::vector<double> dn(n);
+            c->dnorm.download(dn.data(), n, s);
+            FGB_CUDA(cudaStreamSynchronize(s));
+            c->max_dnorm = 0.0;
+            for (double x : dn) c->max_dnorm = std::max(c->max_dnorm, x);
+        }
         *out = c.release();
     });
 }

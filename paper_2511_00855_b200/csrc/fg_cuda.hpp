@@ -111,6 +111,7 @@ struct fg_corpus {
     uint32_t dim = 0, dstride = 0;
     uint32_t max_lnnz = 0, max_snnz = 0;
     uint64_t l_nnz_total4 = 0, s_nnz_total4 = 0;  // padded posting counts / 4
+    uint32_t l_vocab = 0, s_vocab = 0;             // 1 + the largest term id per path
     fgb::DevCorpus dc{};
     fgb::DevBuf<float> dense, l_val, s_val;
     fgb::DevBuf<uint64_t> l_off, s_off, kw_ptr, ent_ptr;
@@ -124,6 +125,7 @@ struct fg_corpus {
     fgb::HostList keywords, entities;
     std::vector<double> sqnorm_h;
     double max_sqnorm = 0.0;  // max over docs of the unit-weight self score (error bounds)
+    double max_dnorm = 0.0;   // max over docs of the dense-row norm (error bounds)
     cudaStream_t stream = nullptr;
 };
 

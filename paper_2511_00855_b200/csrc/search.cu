@@ -1185,14 +1185,26 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.norm_order = ix->norm_order.get();
             pl.entry_count = norm_seeds;
             pl.qflags = d_qflags.get();
-            pl.lcap = hash_capacity(up.max_lnnz);
-            pl.scap = hash_capacity(up.max_snnz);
+            // sparse paths: bitmap + rank lookups for vocabularies up to 64K
+            // terms, filter + hash otherwise (FGB_SEARCH_BITMAP=0: hash only)
+            const char* be = std::getenv("FGB_SEARCH_BITMAP");
+            const bool bitmaps = !(be && be[0] == '0');
+            pl.cap[0] = hash_capacity(up.max_lnnz);
+            pl.cap[1] = hash_capacity(up.max_snnz);
+            pl.vocab[0] = bitmaps && c.l_vocab <= 65536 ? c.l_vocab : 0;
+            pl.vocab[1] = bitmaps && c.s_vocab <= 65536 ? c.s_vocab : 0;
             pl.beamcap = std::max(max_beam, 32u);
             pl.kcap = std::max(max_k, 1u);
             pl.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
+            // |approx - reference| <= eps_coef * |q_w| * max|d| (search_plain.cu):
+            // fp32 partials of <= 4 products (gamma_4 in fp32), fp64 sums of the
+            // partials (depth M) and the reference's own sequential sums (depth N)
             const double N = double(c.dstride) + c.max_lnnz + c.max_snnz + 2;
-            const double M = 4.0 * (((c.dstride >> 2) + 31) / 32) + 4.0 * ((std::max(c.max_lnnz, c.max_snnz) + 127) / 128) + 12;
-            pl.eps_coef = (N + M + 8) * std::ldexp(1.0, -53) * 1.01;
+            const double M = (c.dstride >> 2) + 2.0 * ((std::max(c.max_lnnz, c.max_snnz) + 127) / 128) + 16;
+            const double u32 = std::ldexp(1.0, -24), u64 = std::ldexp(1.0, -53);
+            pl.eps32_coef = 4.0 * u32 / (1.0 - 4.0 * u32) * 1.01 + 1e-30;
+            pl.eps_coef = (N + M + 8) * u64 * 1.01;
+            pl.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
             pl.eps_scale = 1.0;
             if (const char* e = std::getenv("FGB_EPS_SCALE")) pl.eps_scale = std::atof(e);
             pl.prefetch = 2;

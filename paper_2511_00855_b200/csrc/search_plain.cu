@@ -30,6 +30,8 @@
 // pools' contents do not depend on offer order — each expansion's first-time
 // neighbours merge as one sorted batch; deleted nodes enter cand, never topk.
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 #include "query_stage.cuh"
 #include "search_plain.hpp"
@@ -56,30 +58,78 @@ __device__ __forceinline__ bool certain(double da, uint32_t na, double db, uint3
     return ((na & nb & kExact) != 0) || fabs(da - db) > tol;
 }
 
+// One sparse query path staged in shared memory.  Vocabularies up to 64K
+// terms use a bitmap + rank structure (membership = one word test, value
+// index = the word's prefix count + a popcount: branch-free); larger ones a
+// bit filter in front of an open-addressing hash (device_common.cuh).
+struct PathQ {
+    uint32_t on;     // path active for this query (weight != 0, query nnz > 0)
+    uint32_t vocab;  // > 0: bitmap mode over [0, vocab)
+    uint32_t wm1;    // bitmap words - 1
+    const uint32_t* bm;
+    const uint16_t* pre;
+    const float* qv;  // weighted values (fp32, as build_query_vector) in ascending term order
+    const uint32_t* keys;
+    const float* vals;
+    const uint32_t* filt;
+    uint32_t mask;
+};
+
+// The weighted query value of term t (found=false, 0 when absent).
+template <bool kBitmap>
+__device__ __forceinline__ float q_lookup_t(const PathQ& P, uint32_t t, bool& found) {
+    if constexpr (kBitmap) {
+        const uint32_t tw = min(t >> 5, P.wm1);
+        const uint32_t word = P.bm[tw];
+        const uint32_t pre = P.pre[tw];
+        found = t < P.vocab && ((word >> (t & 31)) & 1u);
+        const float q = P.qv[pre + __popc(word & ((1u << (t & 31)) - 1u))];
+        return found ? q : 0.0f;
+    } else {
+        found = false;
+        float q = 0.0f;
+        if (t != kPad && filter_hit(P.filt, 2 * P.mask + 1, t)) found = hash_find(P.keys, P.vals, P.mask, t, q);
+        return found ? q : 0.0f;
+    }
+}
+
+__device__ __forceinline__ float q_lookup(const PathQ& P, uint32_t t, bool& found) {
+    return P.vocab ? q_lookup_t<true>(P, t, found) : q_lookup_t<false>(P, t, found);
+}
+
+struct QueryQ {
+    const float* qd;  // weighted dense query (fp32, zero padded to dstride); nullptr: path off
+    PathQ p[2];       // learned, statistical
+};
+
 // The reference's exact distance — the sequential chains of
 // scoring.cpp:10-99 (dense in index order, then each sparse path's shared
-// terms in ascending order; products exact, one rounding per add).  The rare
-// path (uncertain comparisons, final top-k): few registers.  (Kept inline:
-// an out-of-line call here corrupted live batch registers under sm_100a
-// ptxas 12.9 — tools/smoke_plain.py reproduces it with __noinline__.)
-__device__ __forceinline__ double exact_dist(const DevCorpus* c, SmemQuery sq, uint32_t node) {
+// terms in ascending order; products of fp32 values exact in fp64, one
+// rounding per add).  The rare path (uncertain comparisons, final top-k).
+// (Kept inline: an out-of-line call here corrupted live batch registers
+// under sm_100a ptxas 12.9 — tools/smoke_plain.py reproduced it.)
+__device__ __forceinline__ double exact_dist(const DevCorpus& c, const QueryQ& Q, uint32_t node) {
     double acc = 0.0;
-    if (sq.dense) {
-        const float* row = c->dense + static_cast<uint64_t>(node) * c->dstride;
-        for (uint32_t i = 0; i < c->dstride; ++i) acc = __dadd_rn(acc, __dmul_rn(sq.dense[i], (double)row[i]));
+    if (Q.qd) {
+        const float* row = c.dense + static_cast<uint64_t>(node) * c.dstride;
+        for (uint32_t i = 0; i < c.dstride; ++i)
+            acc = __dadd_rn(acc, __dmul_rn((double)Q.qd[i], (double)row[i]));
     }
+#pragma unroll 1
     for (int path = 0; path < 2; ++path) {
-        const bool learned = path == 0;
-        const uint32_t mask = learned ? sq.lmask : sq.smask;
         double s = 0.0;
-        if (mask) {
-            const uint64_t off = learned ? c->l_off[node] : c->s_off[node];
-            const uint32_t nnz = learned ? c->l_nnz[node] : c->s_nnz[node];
-            const uint32_t* idx = (learned ? c->l_idx : c->s_idx) + off;
-            const float* val = (learned ? c->l_val : c->s_val) + off;
-            for (uint32_t j = 0; j < nnz; ++j)
-                probe_term(idx[j], val[j], learned ? sq.lkeys : sq.skeys, learned ? sq.lvals : sq.svals, mask,
-                           learned ? sq.lfilt : sq.sfilt, s);
+        const bool learned = path == 0;
+        const PathQ P = learned ? Q.p[0] : Q.p[1];
+        if (P.on) {
+            const uint64_t off = learned ? c.l_off[node] : c.s_off[node];
+            const uint32_t nnz = learned ? c.l_nnz[node] : c.s_nnz[node];
+            const uint32_t* idx = (learned ? c.l_idx : c.s_idx) + off;
+            const float* val = (learned ? c.l_val : c.s_val) + off;
+            for (uint32_t j = 0; j < nnz; ++j) {
+                bool f;
+                const float q = q_lookup(P, idx[j], f);
+                if (f) s = __dadd_rn(s, __dmul_rn((double)q, (double)val[j]));
+            }
         }
         acc = __dadd_rn(acc, s);
     }
@@ -87,23 +137,20 @@ __device__ __forceinline__ double exact_dist(const DevCorpus* c, SmemQuery sq, u
 }
 
 // ------------------------------------------------------------ scoring
-// Adds the products of the query terms among 4 postings; the filter tests
-// are branch-free, the hash is probed only for filter hits.
-__device__ __forceinline__ void probe4(const uint4& ii, const float4& vv, const uint32_t* keys, const float* vals,
-                                       const uint32_t* filt, uint32_t mask, double& s) {
-    const uint32_t fm = 2 * mask + 1;
-    const uint32_t t[4] = {ii.x, ii.y, ii.z, ii.w};
-    const float v[4] = {vv.x, vv.y, vv.z, vv.w};
-    uint32_t hits = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) hits |= static_cast<uint32_t>(t[k] != kPad && filter_hit(filt, fm, t[k])) << k;
-    if (hits) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            float q;
-            if (((hits >> k) & 1u) && hash_find(keys, vals, mask, t[k], q)) s = __fma_rn((double)q, (double)v[k], s);
-        }
-    }
+// Exact fp64 products of the query terms among 4 postings, summed in fp64
+// (each product predicated on the lookup hit: no branches, no conversions
+// for misses).
+template <bool kBitmap>
+__device__ __forceinline__ double probe4(const uint4& ii, const float4& vv, const PathQ& P) {
+    bool f0, f1, f2, f3;
+    const float q0 = q_lookup_t<kBitmap>(P, ii.x, f0), q1 = q_lookup_t<kBitmap>(P, ii.y, f1);
+    const float q2 = q_lookup_t<kBitmap>(P, ii.z, f2), q3 = q_lookup_t<kBitmap>(P, ii.w, f3);
+    double s = 0.0;
+    if (f0) s = __fma_rn((double)q0, (double)vv.x, s);
+    if (f1) s = __fma_rn((double)q1, (double)vv.y, s);
+    if (f2) s = __fma_rn((double)q2, (double)vv.z, s);
+    if (f3) s = __fma_rn((double)q3, (double)vv.w, s);
+    return s;
 }
 
 // Reduce-scatter of kSG per-lane partial sums: node k's total (over all 32
@@ -132,10 +179,10 @@ __device__ __forceinline__ double reduce_scatter8(double (&x)[8], uint32_t lane)
 // Warp-cooperative approximate sparse dot of one path for the F nodes held
 // by lanes 0..F-1 ((off4, nnz) each); lane j receives node j's sum.  kSG
 // nodes' first 128 postings (idx + val, coalesced 512 B each) are in flight
-// per round trip; longer rows load the rest synchronously.
-__device__ __forceinline__ double sparse_group(const uint32_t* idx, const float* val, const uint32_t* keys,
-                                               const float* vals, const uint32_t* filt, uint32_t mask,
-                                               uint32_t off4, uint32_t nnz, uint32_t lane, uint32_t F) {
+// per round trip; postings 128.. of longer rows follow in a rolled loop.
+template <bool kBitmap>
+__device__ __noinline__ double sparse_group(const uint32_t* idx, const float* val, const PathQ P, uint32_t off4,
+                                            uint32_t nnz, uint32_t lane, uint32_t F) {
     double mine = 0.0;
     const uint4* i4 = reinterpret_cast<const uint4*>(idx);
     const float4* v4 = reinterpret_cast<const float4*>(val);
@@ -158,26 +205,25 @@ __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float*
         }
         double part[8];
 #pragma unroll
-        for (int k = 0; k < kSG; ++k) {
-            part[k] = 0.0;
-            probe4(ii[k], vv[k], keys, vals, filt, mask, part[k]);
-        }
-        // postings 128.. of long rows (not taken for nnz <= 128)
-#pragma unroll
-        for (int k = 0; k < kSG; ++k) {
-            const uint32_t j = g + k;
-            const uint32_t oj = __shfl_sync(kFull, off4, j & 31);
-            const uint32_t nj_all = __shfl_sync(kFull, nnz, j & 31);
-            const uint32_t nj = j < F ? nj_all : 0u;
-            for (uint32_t base = 32; 4 * base < nj; base += 32)
-                if (4 * (base + lane) < nj)
-                    probe4(__ldg(i4 + oj + base + lane), __ldg(v4 + oj + base + lane), keys, vals, filt, mask,
-                           part[k]);
-        }
+        for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap>(ii[k], vv[k], P);
         const double r = reduce_scatter8(part, lane);
         const uint32_t k = lane - g;  // owner lane g + k takes node k's sum from lane 4k
         const double got = __shfl_sync(kFull, r, (4 * k) & 31);
         if (lane >= g && lane < g + kSG) mine = got;
+    }
+    // postings 128.. of long rows (none for nnz <= 128)
+    uint32_t lm = __ballot_sync(kFull, lane < F && nnz > 128);
+#pragma unroll 1
+    while (lm) {
+        const uint32_t j = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t oj = __shfl_sync(kFull, off4, j), nj = __shfl_sync(kFull, nnz, j);
+        double e = 0.0;
+        for (uint32_t base = 32; 4 * base < nj; base += 32)
+            if (4 * (base + lane) < nj) e += probe4<kBitmap>(__ldg(i4 + oj + base + lane), __ldg(v4 + oj + base + lane), P);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
+        if (lane == j) mine += e;
     }
     return mine;
 }
@@ -194,12 +240,13 @@ __device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, ui
 }
 
 // Warp-cooperative approximate dense dot (coalesced 512-B loads per warp
-// instruction) for every lane-held node in `mask`, two rows per round trip.
+// instruction) for every lane-held node in `mask`, two rows per round trip;
+// fp32 partials of 4 elements, accumulated in fp64.
 template <int NQ4>
-__device__ __forceinline__ double dense_group(const DevCorpus& c, const double* q, uint32_t node, uint32_t lane,
+__device__ __forceinline__ double dense_group(const DevCorpus& c, const float* qd, uint32_t node, uint32_t lane,
                                               uint32_t mask) {
     double mine = 0.0;
-    const double2* q2 = reinterpret_cast<const double2*>(q);
+    const float4* q4 = reinterpret_cast<const float4*>(qd);
     const uint32_t n4 = c.dstride >> 2;
     uint32_t m = mask;
 #pragma unroll 1
@@ -218,15 +265,16 @@ __device__ __forceinline__ double dense_group(const DevCorpus& c, const double* 
         for (int k = 0; k < NQ4; ++k) {
             const uint32_t col = k * 32 + lane;
             if (col < n4) {
-                const double2 x = q2[2 * col], y = q2[2 * col + 1];
-                sa = __fma_rn(x.x, (double)ra[k].x, sa);
-                sa = __fma_rn(x.y, (double)ra[k].y, sa);
-                sa = __fma_rn(y.x, (double)ra[k].z, sa);
-                sa = __fma_rn(y.y, (double)ra[k].w, sa);
-                sb = __fma_rn(x.x, (double)rb[k].x, sb);
-                sb = __fma_rn(x.y, (double)rb[k].y, sb);
-                sb = __fma_rn(y.x, (double)rb[k].z, sb);
-                sb = __fma_rn(y.y, (double)rb[k].w, sb);
+                const float4 q = q4[col];
+                float pa = q.x * ra[k].x, pb = q.x * rb[k].x;
+                pa = __fmaf_rn(q.y, ra[k].y, pa);
+                pb = __fmaf_rn(q.y, rb[k].y, pb);
+                pa = __fmaf_rn(q.z, ra[k].z, pa);
+                pb = __fmaf_rn(q.z, rb[k].z, pb);
+                pa = __fmaf_rn(q.w, ra[k].w, pa);
+                pb = __fmaf_rn(q.w, rb[k].w, pb);
+                sa += (double)pa;
+                sb += (double)pb;
             }
         }
         // reduce-scatter of the pair: lanes 0-15 end with a's sum, 16-31 with b's
@@ -331,7 +379,8 @@ __device__ __forceinline__ uint32_t pool_insert(const Pool& p, uint32_t& size, d
 }
 
 struct PlainMem {
-    unsigned char* stage;
+    float* qd;
+    unsigned char* path[2];  // per sparse path: bitmap (bm, pre, qv) or hash (keys, vals, filt)
     double* cand_d;
     uint32_t* cand_n;
     double* topk_d;
@@ -339,7 +388,16 @@ struct PlainMem {
     uint32_t* br;
 };
 
-__device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
+
+// Bytes of one staged sparse path (PlainLaunch::vocab/cap).
+__host__ __device__ __forceinline__ size_t path_bytes(uint32_t vocab, uint32_t cap) {
+    if (vocab) {
+        const size_t W = (vocab + 31) / 32;
+        return al16(W * 4) + al16(W * 2) + al16(cap * 4);
+    }
+    return al16(cap * 4) + al16(cap * 4) + al16(filter_words(cap) * 4);
+}
 
 __device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch& a) {
     PlainMem m;
@@ -349,7 +407,9 @@ __device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch
         off += al16(bytes);
         return p;
     };
-    m.stage = take(stage_bytes(a.c.dstride, a.lcap, a.scap));
+    m.qd = reinterpret_cast<float*>(take(a.c.dstride * 4));
+    m.path[0] = take(path_bytes(a.vocab[0], a.cap[0]));
+    m.path[1] = take(path_bytes(a.vocab[1], a.cap[1]));
     m.cand_d = reinterpret_cast<double*>(take(a.beamcap * 8));
     m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
     m.cand_n = reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
@@ -358,13 +418,87 @@ __device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch
     return m;
 }
 
+// Stages sparse path `path` of query qi (build_query_vector: fp32 w * v,
+// a zero weight drops the path, corpus.cpp:86-103); returns sum of (w v)^2.
+__device__ double stage_path(const PlainLaunch& a, uint64_t qi, int path, unsigned char* mem, PathQ& P,
+                             uint32_t lane) {
+    const DevQueries& q = a.q;
+    const uint64_t lb = path ? q.s_ptr[qi] : q.l_ptr[qi], le = path ? q.s_ptr[qi + 1] : q.l_ptr[qi + 1];
+    const uint32_t* qidx = path ? q.s_idx : q.l_idx;
+    const float* qval = path ? q.s_val : q.l_val;
+    const float wt = path ? q.weights[qi].z : q.weights[qi].y;
+    const uint32_t vocab = a.vocab[path], cap = a.cap[path];
+    P.on = wt != 0.0f && le > lb;
+    P.vocab = vocab;
+    double ss = 0.0;
+    if (vocab) {
+        const uint32_t W = (vocab + 31) / 32;
+        P.wm1 = W - 1;
+        uint32_t* bm = reinterpret_cast<uint32_t*>(mem);
+        uint16_t* pre = reinterpret_cast<uint16_t*>(mem + al16(W * 4));
+        float* qv = reinterpret_cast<float*>(mem + al16(W * 4) + al16(W * 2));
+        P.bm = bm;
+        P.pre = pre;
+        P.qv = qv;
+        if (!P.on) return 0.0;
+        for (uint32_t i = lane; i < W; i += 32) bm[i] = 0;
+        __syncwarp();
+        for (uint64_t j = lb + lane; j < le; j += 32) {
+            const uint32_t t = qidx[j];
+            if (t < vocab) atomicOr(&bm[t >> 5], 1u << (t & 31));
+        }
+        __syncwarp();
+        // exclusive prefix of the word popcounts over 32 contiguous chunks
+        const uint32_t per = (W + 31) / 32, b0 = min(W, lane * per), b1 = min(W, b0 + per);
+        uint32_t cnt = 0;
+        for (uint32_t i = b0; i < b1; ++i) cnt += __popc(bm[i]);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        uint32_t run = incl - cnt;
+        for (uint32_t i = b0; i < b1; ++i) {
+            pre[i] = static_cast<uint16_t>(run);
+            run += __popc(bm[i]);
+        }
+        __syncwarp();
+        for (uint64_t j = lb + lane; j < le; j += 32) {
+            const uint32_t t = qidx[j];
+            const float v = __fmul_rn(wt, qval[j]);
+            ss += (double)v * (double)v;
+            if (t < vocab) qv[pre[t >> 5] + __popc(bm[t >> 5] & ((1u << (t & 31)) - 1u))] = v;
+        }
+        __syncwarp();
+        return ss;
+    }
+    uint32_t* keys = reinterpret_cast<uint32_t*>(mem);
+    float* vals = reinterpret_cast<float*>(mem + al16(cap * 4));
+    uint32_t* filt = reinterpret_cast<uint32_t*>(mem + 2 * al16(cap * 4));
+    P.keys = keys;
+    P.vals = vals;
+    P.filt = filt;
+    P.mask = cap - 1;
+    if (!P.on) return 0.0;
+    for (uint32_t j = lane; j < cap; j += 32) keys[j] = kEmpty;
+    for (uint32_t j = lane; j < filter_words(cap); j += 32) filt[j] = 0;
+    __syncwarp();
+    for (uint64_t j = lb + lane; j < le; j += 32) {
+        const uint32_t t = qidx[j];
+        const float v = __fmul_rn(wt, qval[j]);
+        ss += (double)v * (double)v;
+        hash_insert(keys, vals, cap - 1, t, v);
+        atomicOr(&filt[(t >> 5) & (filter_words(cap) - 1)], 1u << (t & 31));
+    }
+    __syncwarp();
+    return ss;
+}
+
 template <int NQ4, bool kTime>
 __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ DevCorpus cs;  // for the out-of-line exact scorer
     const uint32_t lane = threadIdx.x & 31;
-    if (lane == 0) cs = a.c;
-    __syncwarp();
     const uint64_t slot = blockIdx.x;
     PlainMem w = carve(smem_raw, a);
     uint32_t* visited = a.visited + slot * a.nwords;
@@ -399,23 +533,35 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             continue;
         }
         const uint32_t K = a.q.k[qi], B = a.q.beam[qi];
-        SmemQuery sq;
-        stage_query(a.q, qi, c.dstride, w.stage, a.lcap, a.scap, lane, 32, sq, [] { __syncwarp(); });
-        // |weighted dense query| (screening) and |weighted query| over all paths (error bound)
+        // ---- stage the weighted query (build_query_vector, corpus.cpp:86-103)
+        QueryQ Q;
         double qd2 = 0.0, qs2 = 0.0;
-        if (sq.dense)
-            for (uint32_t j = lane; j < c.dstride; j += 32) qd2 += sq.dense[j] * sq.dense[j];
-        for (uint32_t j = lane; j < a.lcap; j += 32)
-            if (sq.lmask && sq.lkeys[j] != kEmpty) qs2 += (double)sq.lvals[j] * (double)sq.lvals[j];
-        for (uint32_t j = lane; j < a.scap; j += 32)
-            if (sq.smask && sq.skeys[j] != kEmpty) qs2 += (double)sq.svals[j] * (double)sq.svals[j];
+        {
+            const float wd = a.q.weights[qi].x;
+            const float* x = a.q.dense + qi * a.q.dim;
+            for (uint32_t j = lane; j < c.dstride; j += 32) {
+                const float v = j < a.q.dim ? __fmul_rn(wd, x[j]) : 0.0f;
+                w.qd[j] = v;
+                qd2 += (double)v * (double)v;
+            }
+            Q.qd = wd != 0.0f ? w.qd : nullptr;
+            if (!Q.qd) qd2 = 0.0;
+        }
+        qs2 += stage_path(a, qi, 0, w.path[0], Q.p[0], lane);
+        qs2 += stage_path(a, qi, 1, w.path[1], Q.p[1], lane);
+        __syncwarp();
+        // |weighted dense query| (screening) and |weighted query| over all paths (error bound)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             qd2 += __shfl_xor_sync(kFull, qd2, o);
             qs2 += __shfl_xor_sync(kFull, qs2, o);
         }
         const double qnorm = sqrt(qd2) * (1.0 + 1e-12);
-        const double eps = a.eps_coef * (sqrt(qd2 + qs2) * (1.0 + 1e-10)) * a.max_norm * a.eps_scale + 1e-300;
+        // |approx - reference| <= eps: fp32 dense partials (gamma_4 in fp32 of
+        // sum |q_i d_i| <= |q_d| max|d_dense|) + fp64 sums (depths N, M) of all
+        // products (sum |p| <= |q_w| max|d|, Cauchy-Schwarz)
+        const double eps = (a.eps32_coef * (sqrt(qd2) * (1.0 + 1e-10)) * a.max_dnorm +
+                            a.eps_coef * (sqrt(qd2 + qs2) * (1.0 + 1e-10)) * a.max_norm) * a.eps_scale + 1e-300;
         const double tol = 2.5 * eps;
 
         const Pool topk{w.topk_d, w.topk_n, K};
@@ -483,19 +629,20 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             uint4 mt = make_uint4(0, 0, 0, 0);  // one 16-B record: sparse offsets/lengths, dense norm
             if (mine) {
                 mt = __ldg(c.meta + cn);
-                if (sq.dense && a.prefetch >= 2)
+                if (Q.qd && a.prefetch >= 2)
                     l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
             }
             double L = 0.0, S = 0.0;
 #pragma unroll 1
             for (int path = 0; path < 2; ++path) {
                 const bool learned = path == 0;
-                const uint32_t pm = learned ? sq.lmask : sq.smask;
-                if (!pm) continue;
-                const double r = sparse_group(learned ? c.l_idx : c.s_idx, learned ? c.l_val : c.s_val,
-                                              learned ? sq.lkeys : sq.skeys, learned ? sq.lvals : sq.svals,
-                                              learned ? sq.lfilt : sq.sfilt, pm, learned ? mt.x : mt.y,
-                                              learned ? (mt.z & 0xFFFFu) : (mt.z >> 16), lane, F);
+                const PathQ P = learned ? Q.p[0] : Q.p[1];  // (a select, not a dynamic index)
+                if (!P.on) continue;
+                const uint32_t* pidx = learned ? c.l_idx : c.s_idx;
+                const float* pval = learned ? c.l_val : c.s_val;
+                const uint32_t off4 = learned ? mt.x : mt.y, pnnz = learned ? (mt.z & 0xFFFFu) : (mt.z >> 16);
+                const double r = P.vocab ? sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F)
+                                         : sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
                 if (learned)
                     L = r;
                 else
@@ -507,14 +654,14 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             bool keep = mine;
             if (mine && csize == B && tsize == K) {
                 const double floor = fmin(-w.cand_d[csize - 1], -w.topk_d[tsize - 1]) - 4.0 * eps;
-                const double dn = sq.dense ? (double)__uint_as_float(mt.w) : 0.0;
-                const double ub = score_upper_bound(sq.dense ? qnorm : 0.0, dn, L, S) + 2.0 * eps;
+                const double dn = Q.qd ? (double)__uint_as_float(mt.w) : 0.0;
+                const double ub = score_upper_bound(Q.qd ? qnorm : 0.0, dn, L, S) + 2.0 * eps;
                 keep = !(ub < floor);
             }
             const uint32_t km = __ballot_sync(kFull, keep);
-            if (keep && sq.dense && a.prefetch == 1)
+            if (keep && Q.qd && a.prefetch == 1)
                 l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
-            const double D = sq.dense ? dense_group<NQ4>(c, sq.dense, cn, lane, km) : 0.0;
+            const double D = Q.qd ? dense_group<NQ4>(c, Q.qd, cn, lane, km) : 0.0;
             phase_end(kPlainPhDense);
             const uint32_t m = __popc(km);
             if (m == 0) continue;
@@ -577,7 +724,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                 const uint32_t fxm = __ballot_sync(kFull, fix);
                 if (!fxm && !ntm && !ncm) break;
                 if (fix) {
-                    d = exact_dist(&cs, sq, n & kId);
+                    d = exact_dist(c, Q, n & kId);
                     n |= kExact;
                 }
                 resolved += __popc(fxm);
@@ -594,7 +741,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                         const int i = static_cast<int>(__shfl_sync(kFull, rk, j)) - 4 + static_cast<int>(lane);
                         const bool pf = lane < 8 && i >= 0 && i < static_cast<int>(sz) && !(P.n[i] & kExact);
                         if (pf) {
-                            P.d[i] = exact_dist(&cs, sq, P.n[i] & kId);
+                            P.d[i] = exact_dist(c, Q, P.n[i] & kId);
                             P.n[i] |= kExact;
                         }
                         resolved += __popc(__ballot_sync(kFull, pf));
@@ -612,7 +759,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
         // (keyword_postfilter with no required keywords: topk as is, search.cpp:100-139)
         for (uint32_t i = lane; i < tsize; i += 32) {
             if (!(w.topk_n[i] & kExact)) {
-                w.topk_d[i] = exact_dist(&cs, sq, w.topk_n[i] & kId);
+                w.topk_d[i] = exact_dist(c, Q, w.topk_n[i] & kId);
                 ++final_exact;
             }
             a.r_node[static_cast<uint64_t>(qi) * a.hit_stride + i] = w.topk_n[i] & kId;
@@ -693,9 +840,9 @@ const void* kernel_for(int v) {
 
 size_t plain_warp_smem(const PlainLaunch& a) {
     if (nq4_of(a) == 0) return 0;  // dense rows wider than 1,024 floats: general kernel
-    auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
-    const size_t b = al(stage_bytes(a.c.dstride, a.lcap, a.scap)) + al(a.beamcap * 8) + al(a.kcap * 8) +
-                     al(a.beamcap * 4) + al(a.kcap * 4) + al(32 * 4);
+    const size_t b = al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0])) +
+                     al16(path_bytes(a.vocab[1], a.cap[1])) + al16(a.beamcap * 8) + al16(a.kcap * 8) +
+                     al16(a.beamcap * 4) + al16(a.kcap * 4) + al16(32 * 4);
     return b <= 227 * 1024 ? b : 0;
 }
 
@@ -707,6 +854,8 @@ uint64_t plain_slots(const PlainLaunch& a, uint64_t nq, int device) {
     FGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem));
     FGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     per_sm = std::max(per_sm, 1);
+    if (const char* e = std::getenv("FGB_SEARCH_WARPS_PER_SM"))  // dev: occupancy sweeps
+        per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     return std::max<uint64_t>(1, std::min<uint64_t>(nq, static_cast<uint64_t>(sms) * per_sm));
 }
 

@@ -14,10 +14,13 @@ struct PlainLaunch {
     const uint32_t* norm_order;
     uint32_t entry_count;
     const uint8_t* qflags;      // QF_VALID | QF_FALLBACK
-    uint32_t lcap, scap;        // staged sparse hash capacities
+    uint32_t vocab[2];          // per sparse path (learned, statistical): bitmap width, 0 = hash
+    uint32_t cap[2];            // per sparse path: hash capacity / staged value slots
     uint32_t beamcap, kcap;     // max beam / k in the batch
     double max_norm;            // >= sqrt(max sqnorm) of the corpus
-    double eps_coef;            // error-bound coefficient (see search_plain.cu)
+    double max_dnorm;           // >= max dense-row norm of the corpus
+    double eps_coef;            // fp64 error-bound coefficient (see search_plain.cu)
+    double eps32_coef;          // fp32 dense-partial error coefficient
     uint32_t* visited;          // per-warp exact bitsets, nwords each
     uint64_t nwords;
     uint32_t* touched;          // per-warp touched lists, tcap each

@@ -66,6 +66,8 @@ def test_plain_c2_shape_identical(c2_small, ref, beam, entry):
     same(g, ref.batch_query(rix, q, entry_count=entry, threads=os.cpu_count() or 1))
     with env(FGB_SEARCH_PLAIN=0):  # the general (sequential-chain) kernel agrees too
         same(fg.batch_query(gix, q, entry_count=entry), g)
+    with env(FGB_SEARCH_BITMAP=0):  # hash lookups instead of the learned-path bitmap
+        same(fg.batch_query(gix, q, entry_count=entry), g)
 
 
 def test_plain_forced_exact_resolution(c2_small, ref):
