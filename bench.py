@@ -167,9 +167,17 @@ def main():
     corpus, kg, _ = synth.generate_corpus(p, 0)
     t_gen = time.time() - t0
     dc = fg.DeviceCorpus(corpus, device=local)
+    # construction: vertex-range sharded over the ranks (NCCL all-gathers per
+    # NN-Descent pass); one rank builds alone
+    from paper_2511_00855_b200.shard import build_comm
+    comm = build_comm(world, rank, local)
+    group.barrier()
     t0 = time.time()
-    ix = fg.build_hybrid_index(dc, kg, **BUILD)
-    build_s = time.time() - t0
+    if comm is not None:
+        ix = fg.build_hybrid_index_sharded(dc, kg, comm=comm, **BUILD)
+    else:
+        ix = fg.build_hybrid_index(dc, kg, **BUILD)
+    build_s = group.max(time.time() - t0)
     stages = ix.build_times()
 
     queries = synth.synth_queries(p, args.queries)
@@ -246,7 +254,7 @@ def main():
                         "(vocab 30522), dense+sparse fusion, per-query simplex weights",
             "docs": corpus.n, "queries_per_step": queries.count, "queries_per_gpu": hi - lo,
             "k": 10, "beam": beam, "entry_count": entry, "build": BUILD,
-            "parallelism": f"query-shard x{world}, index replicated",
+            "parallelism": f"query-shard x{world}, index replicated; build vertex-range x{world} (NCCL all-gather)",
             "l2": "flushed (256 MiB write) before each timed step; corpus 4 GB > L2",
         },
         "recall_at_10": next((s["recall"] for s in sweep if s["beam"] == beam and s["entry"] == entry), None),

@@ -197,6 +197,7 @@ typedef struct fg_synth_params {
 typedef struct fg_host_corpus fg_host_corpus; /* generator output, library-owned */
 typedef struct fg_corpus fg_corpus;           /* device mirror of a DocumentStore */
 typedef struct fg_index fg_index;             /* device-resident HybridIndex */
+typedef struct fg_comm fg_comm;               /* NCCL communicator of a sharded build */
 
 /* ------------------------------------------------------------------------ */
 /* Errors and devices                                                         */
@@ -311,6 +312,29 @@ int fg_index_export(const fg_index* ix, uint32_t* semantic, uint64_t* keyword_pt
  * [0] knn, [1] refine, [2] logical+entity map, [3] norm order, [4] total. */
 int fg_index_build_times(const fg_index* ix, double* seconds5);
 int fg_index_free(fg_index* ix);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU construction: vertex-range sharding              */
+/* ------------------------------------------------------------------------ */
+
+/* One process per GPU.  Rank 0 creates the id, the caller broadcasts it (any
+ * host channel, e.g. torch.distributed), every rank then calls fg_comm_init.
+ * NCCL is loaded at run time (libnccl.so.2). */
+#define FG_COMM_ID_BYTES 128
+int fg_comm_unique_id(uint8_t* id /* FG_COMM_ID_BYTES */);
+int fg_comm_init(int nranks, int rank, const uint8_t* id, int device, fg_comm** out);
+int fg_comm_free(fg_comm* comm);
+
+/* build_hybrid_index (index.hpp:60-61) sharded by vertex range: rank r runs
+ * the NN-Descent passes and the per-node refinery for nodes
+ * [r*ceil(n/G), (r+1)*ceil(n/G)), all-gathering each pass's lists and the
+ * refined lists over NCCL; merge_reverse_edges, logical edges and the norm
+ * order are replicated.  The index is identical on every rank and identical
+ * to fg_index_build's (the passes are double-buffered, knn_graph.cpp:91).
+ * comm == NULL with sim_ranks = G > 1 runs all G ranges in this process (no
+ * collective) — the partition logic on one GPU, for parity tests. */
+int fg_index_build_sharded(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* params,
+                           fg_comm* comm, uint32_t sim_ranks, fg_index** out);
 
 /* ------------------------------------------------------------------------ */
 /* Batched beam search (K5) and exhaustive truth (K6)                       */

@@ -228,7 +228,15 @@ Lists knn_init(const Store& s, uint32_t k, uint64_t seed) {  // knn_graph.cpp:26
     return L;
 }
 
-uint64_t knn_pass(const Store& s, Lists& L, uint32_t k) {  // knn_graph.cpp:75-148
+// knn_graph.cpp:75-148 restricted to nodes [lo, hi): rows outside the range
+// of `L` are left as they are (the test harness of the vertex-range sharded
+// build gathers the ranges; the pass is double-buffered, so the union of the
+// ranges equals the full pass).
+uint64_t knn_pass_range(const Store& s, Lists& L, uint32_t k, uint64_t lo, uint64_t hi);
+
+uint64_t knn_pass(const Store& s, Lists& L, uint32_t k) { return knn_pass_range(s, L, k, 0, L.size()); }
+
+uint64_t knn_pass_range(const Store& s, Lists& L, uint32_t k, uint64_t lo, uint64_t hi) {
     const uint64_t n = L.size();
     Lists R(n);
     for (uint64_t u = 0; u < n; ++u)
@@ -237,9 +245,9 @@ uint64_t knn_pass(const Store& s, Lists& L, uint32_t k) {  // knn_graph.cpp:75-1
         std::sort(r.begin(), r.end(), better);
         if (r.size() > k) r.resize(k);
     }
-    Lists next(n);
+    Lists next = L;
     uint64_t replaced = 0;
-    for (uint64_t u = 0; u < n; ++u) {
+    for (uint64_t u = lo; u < hi; ++u) {
         std::map<uint32_t, bool> pool;  // candidate -> some path fresh
         auto via = [&](const Entry& h1) {
             for (const auto* side : {&L[h1.id], &R[h1.id]})
@@ -734,6 +742,13 @@ int fgo_knn_iterate(void* h, fg_knn_lists* l, unsigned, uint64_t* changed) {
     return run([&] {
         Lists L = knn_in(l);
         *changed = knn_pass(*static_cast<Store*>(h), L, l->k);
+        knn_out(L, l);
+    });
+}
+int fgo_knn_iterate_range(void* h, fg_knn_lists* l, uint64_t lo, uint64_t hi, uint64_t* changed) {
+    return run([&] {
+        Lists L = knn_in(l);
+        *changed = knn_pass_range(*static_cast<Store*>(h), L, l->k, lo, hi);
         knn_out(L, l);
     });
 }

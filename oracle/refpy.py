@@ -57,6 +57,7 @@ class _Base:
             "pair_scores": (C.c_int, [C.c_void_p, A.u32p, A.u32p, C.c_uint64, A.f64p]),
             "knn_init": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint, P(A.KnnLists)]),
             "knn_iterate": (C.c_int, [C.c_void_p, P(A.KnnLists), C.c_uint, A.u64p]),
+            "knn_iterate_range": (C.c_int, [C.c_void_p, P(A.KnnLists), C.c_uint64, C.c_uint64, A.u64p]),
             "knn_build": (C.c_int, [C.c_void_p, P(A.KnnParams), C.c_uint, P(A.KnnLists)]),
             "refine": (C.c_int, [C.c_void_p, P(A.KnnLists), P(A.RefineParams), C.c_uint,
                                  P(A.Refined), P(A.RefineTrace)]),
@@ -142,6 +143,14 @@ class _Base:
         s = A.knn_struct(ids, sc, fr)
         ch = C.c_uint64()
         self._check(self._knn_iterate(store.h, C.byref(s), threads, C.byref(ch)))
+        return ids, sc, fr, ch.value
+
+    def knn_iterate_range(self, store, ids, sc, fr, lo, hi):
+        """One pass for nodes [lo, hi) only (other rows returned unchanged)."""
+        ids, sc, fr = ids.copy(), sc.copy(), fr.copy()
+        s = A.knn_struct(ids, sc, fr)
+        ch = C.c_uint64()
+        self._check(self._knn_iterate_range(store.h, C.byref(s), lo, hi, C.byref(ch)))
         return ids, sc, fr, ch.value
 
     def knn_build(self, store, n, k, max_iterations=12, convergence=0.01, seed=42, threads=1):

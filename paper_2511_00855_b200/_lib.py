@@ -64,6 +64,11 @@ def _declare(lib):
         "fg_index_export": (C.c_int, [C.c_void_p, A.u32p, A.u64p, A.u32p, A.u64p, A.u32p,
                                       A.u32p]),
         "fg_index_build_times": (C.c_int, [C.c_void_p, A.f64p]),
+        "fg_comm_unique_id": (C.c_int, [A.u8p]),
+        "fg_comm_init": (C.c_int, [C.c_int, C.c_int, A.u8p, C.c_int, P(C.c_void_p)]),
+        "fg_comm_free": (C.c_int, [C.c_void_p]),
+        "fg_index_build_sharded": (C.c_int, [C.c_void_p, P(A.KgView), P(A.BuildParams), C.c_void_p,
+                                             C.c_uint32, P(C.c_void_p)]),
         "fg_index_free": (C.c_int, [C.c_void_p]),
         "fg_batch_query": (C.c_int, [C.c_void_p, P(A.QueryView), P(A.SearchOpts),
                                      P(A.SearchResults)]),

@@ -116,6 +116,7 @@ struct PassArgs {
     unsigned long long* changed;
     uint32_t pool_cap;  // power of two
     uint32_t lcap, scap;
+    uint64_t lo;        // first node of this launch (vertex-range sharding)
 };
 
 __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uint32_t mask,
@@ -129,11 +130,11 @@ __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uin
     if (fresh) atomicOr(&fbits[s >> 5], 1u << (s & 31));
 }
 
-// One NN-Descent pass for node u = blockIdx.x.
+// One NN-Descent pass for node u = lo + blockIdx.x.
 __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
-    const uint64_t u = blockIdx.x;
+    const uint64_t u = a.lo + blockIdx.x;
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     SmemQuery sq;
     unsigned char* p = smem + ((doc_stage_bytes(a.c.dstride, a.lcap, a.scap) + 15) & ~size_t(15));
@@ -335,17 +336,18 @@ void knn_init_device(const fg_corpus& c, uint32_t k, uint64_t seed, DevKnn& g, c
     FGB_LAUNCH("knn_init_score_kernel");
 }
 
-uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
+// Reverse lists of the snapshot g (knn_graph.cpp:78-89): R[v] = the first
+// min(k, |{u : v in L[u]}|) sources by (score desc, u asc), with freshness.
+void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s) {
     const uint64_t n = g.n;
     const uint32_t k = g.k;
     const uint64_t m = n * k;
     if (m >= 0xFFFFFFFFull) throw Error("invalid-argument", "n*k exceeds 2^32 entries");
-
-    // ---- reverse lists (knn_graph.cpp:78-89)
     DevBuf<uint64_t> keys_a(m), keys_b(m);
     DevBuf<uint32_t> vals_a(m), vals_b(m), tkeys_a(m), tkeys_b(m), cnt(n), start(n);
-    DevBuf<uint32_t> rids(m), rcnt(n);
-    DevBuf<uint8_t> rfresh(m);
+    R.ids.alloc(m);
+    R.cnt.alloc(n);
+    R.fresh.alloc(m);
     cnt.zero(s);
     const unsigned gb = (unsigned)((m + 255) / 256);
     score_keys_kernel<<<gb, 256, 0, s>>>(g.scores.get(), m, keys_a.get(), vals_a.get());
@@ -370,31 +372,38 @@ uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
     tb = temp.size();
     FGB_CUDA(cub::DeviceScan::ExclusiveSum(temp.get(), tb, cnt.get(), start.get(), (int)n, s));
     reverse_fill_kernel<<<gb, 256, 0, s>>>(n, k, vals_a.get(), cnt.get(), start.get(),
-                                           g.fresh.get(), rids.get(), rfresh.get(), rcnt.get());
+                                           g.fresh.get(), R.ids.get(), R.fresh.get(), R.cnt.get());
     FGB_LAUNCH("reverse_fill_kernel");
-    keys_a.release();
-    keys_b.release();
-    vals_b.release();
-    tkeys_a.release();
-    tkeys_b.release();
-    temp.release();
+}
 
-    // ---- per-node two-hop join (knn_graph.cpp:91-142)
-    DevKnn next;
-    next.alloc(n, k);
-    DevBuf<unsigned long long> changed(1);
-    changed.zero(s);
+// The per-node two-hop join (knn_graph.cpp:91-142) for nodes [lo, hi) of the
+// snapshot g (with its reverse lists R) into rows [lo, hi) of next; adds the
+// number of replaced entries to *d_changed (device).
+void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, uint64_t lo, uint64_t hi,
+                    DevKnn& next, unsigned long long* d_changed, cudaStream_t s) {
+    if (hi <= lo) return;
+    const uint32_t k = g.k;
     const uint32_t lcap = hash_capacity(c.max_lnnz), scap = hash_capacity(c.max_snnz);
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
-               rids.get(),     rfresh.get(), rcnt.get(),   next.ids.get(), next.scores.get(),
-               next.fresh.get(), changed.get(), pool_capacity(n, k), lcap, scap};
+               R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
+               next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo};
     const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap);
     if (sm > 227 * 1024)
         throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
                                             std::to_string(sm) + " B)");
     FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    knn_pass_kernel<<<(unsigned)n, kPassThreads, sm, s>>>(a);
+    knn_pass_kernel<<<(unsigned)(hi - lo), kPassThreads, sm, s>>>(a);
     FGB_LAUNCH("knn_pass_kernel");
+}
+
+uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
+    ReverseLists R;
+    knn_reverse_lists(g, R, s);
+    DevKnn next;
+    next.alloc(g.n, g.k);
+    DevBuf<unsigned long long> changed(1);
+    changed.zero(s);
+    knn_pass_range(c, g, R, 0, g.n, next, changed.get(), s);
     unsigned long long h_changed = 0;
     changed.download(&h_changed, 1, s);
     FGB_CUDA(cudaStreamSynchronize(s));

@@ -21,8 +21,19 @@ struct DevKnn {
     }
 };
 
+// Reverse lists of a snapshot (knn_graph.cpp:78-89).
+struct ReverseLists {
+    DevBuf<uint32_t> ids;    // n x k
+    DevBuf<uint32_t> cnt;    // n
+    DevBuf<uint8_t> fresh;   // n x k
+};
+
 // init_random_graph (knn_graph.cpp:52-73) into g (allocated n x k).
 void knn_init_device(const fg_corpus& c, uint32_t k, uint64_t seed, DevKnn& g, cudaStream_t s);
+void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s);
+// The two-hop join for nodes [lo, hi) of g into the same rows of next.
+void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, uint64_t lo, uint64_t hi,
+                    DevKnn& next, unsigned long long* d_changed, cudaStream_t s);
 // nn_descent_iterate (knn_graph.cpp:75-148), in place; returns #replaced.
 uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s);
 // build_knn_graph (knn_graph.cpp:150-166); returns the number of passes run.
@@ -44,5 +55,12 @@ struct RefineOut {
 // refine_graph (refine.cpp:167-217).
 void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool per_neighbour,
                    RefineOut& out, cudaStream_t s);
+// Its two halves: the per-node refinery (ranked candidates, detours, IP prune +
+// keyword recycling) for nodes [lo, hi) — `out` allocated for all n — and
+// merge_reverse_edges + keyword disjointness over every node (needs all kept lists).
+void refine_alloc(const DevKnn& g, uint32_t degree, RefineOut& out, cudaStream_t s);
+void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint64_t lo, uint64_t hi,
+                  RefineOut& out, cudaStream_t s);
+void refine_merge(uint64_t n, RefineOut& out, cudaStream_t s);
 
 }  // namespace fgb

@@ -75,12 +75,13 @@ struct RefineArgs {
     uint32_t* rec_count;   // n
     uint32_t kwcap;        // kept-keyword hash capacity (power of two)
     uint32_t ukw_cap;      // max keyword list length
+    uint64_t lo;           // first node of this launch (vertex-range sharding)
 };
 
 __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
-    const uint64_t u = blockIdx.x;
+    const uint64_t u = a.lo + blockIdx.x;
     const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     double* P = reinterpret_cast<double*>(smem);             // k*k
     double* csc = P + k * k;                                 // k
@@ -362,8 +363,7 @@ __global__ void merge_reverse_kernel(uint64_t n, uint32_t k, uint32_t degree, co
 
 }  // namespace
 
-void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool per_neighbour,
-                   RefineOut& out, cudaStream_t s) {
+void refine_alloc(const DevKnn& g, uint32_t degree, RefineOut& out, cudaStream_t s) {
     const uint64_t n = g.n;
     const uint32_t k = g.k;
     if (degree == 0) throw Error("invalid-k", "degree must be positive");
@@ -381,7 +381,12 @@ void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool pe
     out.kept.alloc(n * degree);
     out.kept_count.alloc(n);
     FGB_CUDA(cudaMemsetAsync(out.semantic.get(), 0xFF, n * degree * 4, s));
+}
 
+void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint64_t lo, uint64_t hi,
+                  RefineOut& out, cudaStream_t s) {
+    if (hi <= lo) return;
+    const uint32_t k = g.k, degree = out.degree;
     uint32_t max_kw = 0;
     for (size_t i = 0; i < c.keywords.rows(); ++i)
         max_kw = std::max<uint32_t>(max_kw, static_cast<uint32_t>(c.keywords.len(i)));
@@ -389,15 +394,18 @@ void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool pe
     while (kwcap < 2ull * max_kw * std::min(degree, k)) kwcap <<= 1;
     RefineArgs a{c.dc, k, degree, per_neighbour ? 1 : 0, g.ids.get(), g.scores.get(),
                  out.ordered.get(), out.ordered_sc.get(), out.detours.get(), out.kept.get(),
-                 out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw};
+                 out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw, lo};
     const size_t sm = static_cast<size_t>(k) * k * 8 + k * 8 + static_cast<size_t>(k) * kTileStride * 4 +
                       5 * k * 4 + static_cast<size_t>(kwcap) * 4 + static_cast<size_t>(max_kw) * 4 + 16;
     if (sm > 227 * 1024)
         throw Error("invalid-k", "refinery shared memory exceeds the SM (" + std::to_string(sm) + " B)");
     FGB_CUDA(cudaFuncSetAttribute(refine_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    refine_node_kernel<<<(unsigned)n, kRefineThreads, sm, s>>>(a);
+    refine_node_kernel<<<(unsigned)(hi - lo), kRefineThreads, sm, s>>>(a);
     FGB_LAUNCH("refine_node_kernel");
+}
 
+void refine_merge(uint64_t n, RefineOut& out, cudaStream_t s) {
+    const uint32_t k = out.k, degree = out.degree;
     // ---- keepers sorted by (target, position, keeper) (refine.cpp:127-133)
     const uint64_t m = n * degree;
     DevBuf<uint32_t> pos_a(m), pos_b(m), vals_a(m), vals_b(m), tkey_a(m), tkey_b(m), cnt(n + 1),
@@ -431,6 +439,13 @@ void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool pe
         out.ordered.get(), out.semantic.get(), out.keyword.get(), out.kw_count.get());
     FGB_LAUNCH("merge_reverse_kernel");
     FGB_CUDA(cudaStreamSynchronize(s));
+}
+
+void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool per_neighbour,
+                   RefineOut& out, cudaStream_t s) {
+    refine_alloc(g, degree, out, s);
+    refine_nodes(c, g, per_neighbour, 0, g.n, out, s);
+    refine_merge(g.n, out, s);
 }
 
 }  // namespace fgb

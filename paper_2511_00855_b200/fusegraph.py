@@ -24,7 +24,8 @@ from ._lib import Error, check, lib
 __all__ = [
     "Error", "DeviceCorpus", "HybridIndex", "build_query_vector", "batch_scores", "pair_scores",
     "init_random_graph", "nn_descent_iterate", "build_knn_graph", "refine_graph",
-    "build_hybrid_index", "batch_query", "search", "brute_force_topk", "recall_at_k",
+    "build_hybrid_index", "build_hybrid_index_sharded", "Comm", "batch_query", "search",
+    "brute_force_topk", "recall_at_k",
 ]
 
 
@@ -214,6 +215,51 @@ def build_hybrid_index(dc: DeviceCorpus, kg: A.KG | None = None, degree=32, knn_
                       int(per_neighbour_keyword_check))
     kv = (kg or A.KG()).view()
     check(lib().fg_index_build(dc.h, C.byref(kv), C.byref(p), C.byref(h)))
+    return HybridIndex(dc, h)
+
+
+class Comm:
+    """NCCL communicator of a sharded build (fg_comm_*): one per process/GPU."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = np.zeros(Comm.ID_BYTES, np.uint8)
+        check(lib().fg_comm_unique_id(A.ptr(buf, A.u8p)))
+        return buf.tobytes()
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: int = 0):
+        buf = np.frombuffer(uid, np.uint8).copy()
+        h = C.c_void_p()
+        check(lib().fg_comm_init(nranks, rank, A.ptr(buf, A.u8p), device, C.byref(h)))
+        self.h, self.rank, self.size = h, rank, nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fg_comm_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_hybrid_index_sharded(dc: DeviceCorpus, kg: A.KG | None = None, comm: Comm | None = None,
+                               sim_ranks: int = 1, degree=32, knn_k=32, knn_iterations=10, seed=42,
+                               logical_cap=64, default_entity_hops=2,
+                               per_neighbour_keyword_check=False) -> HybridIndex:
+    """build_hybrid_index sharded by vertex range over `comm`'s
+    ranks (one GPU each, NCCL all-gathers), or — comm None — over `sim_ranks`
+    ranges computed in this process.  Identical to build_hybrid_index."""
+    h = C.c_void_p()
+    p = A.BuildParams(degree, knn_k, knn_iterations, seed, logical_cap, default_entity_hops,
+                      int(per_neighbour_keyword_check))
+    kv = (kg or A.KG()).view()
+    check(lib().fg_index_build_sharded(dc.h, C.byref(kv), C.byref(p), comm.h if comm else None,
+                                       sim_ranks, C.byref(h)))
     return HybridIndex(dc, h)
 
 

@@ -57,3 +57,22 @@ class Group:
         t = torch.tensor([float(x)], dtype=torch.float64, device=self.device)
         dist.broadcast(t, src)
         return float(t.item())
+
+
+def build_comm(world: int, rank: int, device: int):
+    """The library's NCCL communicator for a sharded build (fg_comm_init):
+    rank 0 draws the unique id, torch.distributed broadcasts it (any backend)."""
+    from .fusegraph import Comm
+    if world == 1:
+        return None
+    import torch.distributed as dist
+    box = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return Comm(world, rank, box[0], device)
+
+
+def vertex_ranges(n: int, world: int) -> list[tuple[int, int]]:
+    """Node ranges of the sharded build: rank r owns [r*cn, min(n, (r+1)*cn)),
+    cn = ceil(n / world) (fg_index_build_sharded, include/fg_b200.h)."""
+    cn = (n + world - 1) // world
+    return [(min(n, r * cn), min(n, (r + 1) * cn)) for r in range(world)]
