@@ -102,6 +102,11 @@ void logical_for(const fg_corpus& c, uint32_t node, const HostKg& kg,
 
 }  // namespace
 
+__global__ void gather_meta_kernel(const uint4* meta, const uint32_t* ids, uint64_t m, uint4* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < m) out[i] = meta[ids[i]];
+}
+
 void index_finish(fg_index& ix, const fg_kg_view* kgv) {
     fg_corpus& c = *ix.corpus;
     cudaStream_t s = c.stream;
@@ -175,6 +180,17 @@ void index_finish(fg_index& ix, const fg_kg_view* kgv) {
         });
     }
     ix.norm_order.upload(ix.norm_order_h, s);
+    if (c.dc.meta && n) {
+        const uint64_t me = n * ix.degree;
+        ix.edge_meta.alloc(me);
+        gather_meta_kernel<<<(unsigned)((me + 255) / 256), 256, 0, s>>>(c.dc.meta, ix.semantic.get(), me,
+                                                                         ix.edge_meta.get());
+        FGB_LAUNCH("gather_meta_kernel");
+        ix.norm_meta.alloc(n);
+        gather_meta_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c.dc.meta, ix.norm_order.get(), n,
+                                                                        ix.norm_meta.get());
+        FGB_LAUNCH("gather_meta_kernel");
+    }
     ix.max_kw_edges = 0;
     for (size_t u = 0; u < ix.keyword_h.rows(); ++u)
         ix.max_kw_edges = std::max<uint32_t>(ix.max_kw_edges, static_cast<uint32_t>(ix.keyword_h.len(u)));

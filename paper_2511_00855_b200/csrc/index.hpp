@@ -18,6 +18,11 @@ struct fg_index {
     fgb::DevBuf<uint64_t> lg_ptr;    // logical edges CSR, uint4 = (source, relation, target, via)
     fgb::DevBuf<uint4> lg;
     fgb::DevBuf<uint32_t> norm_order;
+    // gather records (DevCorpus::meta) of every semantic edge's target and of
+    // the nodes in norm order: the plain search reads them coalesced with the
+    // adjacency list instead of one dependent scattered load per candidate
+    fgb::DevBuf<uint4> edge_meta;   // n x degree
+    fgb::DevBuf<uint4> norm_meta;   // n
     fgb::DevBuf<uint64_t> kg_ptr;    // entity -> sorted unique related entities
     fgb::DevBuf<uint32_t> kg_nbr;
     uint32_t kg_rows = 0;

@@ -1175,7 +1175,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         // ---- plain batches (no entity context, no required keywords): the
         // certified-approximate kernel (search_plain.cu), bit-identical results
         const char* pe = std::getenv("FGB_SEARCH_PLAIN");
-        const bool plain_ok = !any_ctx && !any_req && (!pe || pe[0] != '0') && n < kId30 && c.dc.meta;
+        const bool plain_ok = !any_ctx && !any_req && (!pe || pe[0] != '0') && n < kId30 && c.dc.meta && ix->edge_meta.get();
         if (plain_ok && nq) {
             PlainLaunch pl{};
             pl.c = c.dc;
@@ -1183,6 +1183,8 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.degree = ix->degree;
             pl.q = up.dq;
             pl.norm_order = ix->norm_order.get();
+            pl.edge_meta = ix->edge_meta.get();
+            pl.norm_meta = ix->norm_meta.get();
             pl.entry_count = norm_seeds;
             pl.qflags = d_qflags.get();
             // sparse paths: bitmap + rank lookups for vocabularies up to 64K

@@ -576,11 +576,15 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             // (search.cpp:205-216), then the neighbours of the first
             // unexpanded cand entry, 32 at a time (search.cpp:218-264)
             uint32_t node = 0;
+            uint4 nm = make_uint4(0, 0, 0, 0);  // the node's gather record, loaded with its id
             bool v = false;
             if (seed_next < a.entry_count) {
                 const uint32_t i = seed_next + lane;
                 v = i < a.entry_count;
-                if (v) node = a.norm_order[i];
+                if (v) {
+                    node = a.norm_order[i];
+                    nm = __ldg(a.norm_meta + i);
+                }
                 seed_next += 32;
             } else {
                 if (adj_b >= a.degree) {
@@ -604,7 +608,11 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                 }
                 const uint32_t j = adj_b + lane;
                 v = j < a.degree;
-                if (v) node = a.semantic[static_cast<uint64_t>(adj_u) * a.degree + j];
+                if (v) {
+                    const uint64_t e = static_cast<uint64_t>(adj_u) * a.degree + j;
+                    node = a.semantic[e];
+                    nm = __ldg(a.edge_meta + e);
+                }
                 adj_b += 32;
             }
             // first-time test (a repeated neighbour loses the test-and-set to
@@ -621,17 +629,19 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             // ---- score the F fresh nodes, compacted into lanes 0..F-1
             const uint32_t F = __popc(fm);
             const uint32_t src = __fns(fm, 0, lane + 1);
-            const uint32_t cn = __shfl_sync(kFull, node, src < 32 ? src : 0);
+            const uint32_t sl = src < 32 ? src : 0;
+            const uint32_t cn = __shfl_sync(kFull, node, sl);
+            uint4 mt;  // one 16-B record: sparse offsets/lengths, dense norm
+            mt.x = __shfl_sync(kFull, nm.x, sl);
+            mt.y = __shfl_sync(kFull, nm.y, sl);
+            mt.z = __shfl_sync(kFull, nm.z, sl);
+            mt.w = __shfl_sync(kFull, nm.w, sl);
             const bool mine = lane < F;
             if (mine && ntouched + lane < a.tcap) touched[ntouched + lane] = cn;
             ntouched += F;
             scored += F;
-            uint4 mt = make_uint4(0, 0, 0, 0);  // one 16-B record: sparse offsets/lengths, dense norm
-            if (mine) {
-                mt = __ldg(c.meta + cn);
-                if (Q.qd && a.prefetch >= 2)
-                    l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
-            }
+            if (mine && Q.qd && a.prefetch >= 2)
+                l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
             double L = 0.0, S = 0.0;
 #pragma unroll 1
             for (int path = 0; path < 2; ++path) {

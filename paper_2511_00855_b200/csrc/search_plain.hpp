@@ -12,6 +12,8 @@ struct PlainLaunch {
     uint32_t degree;
     DevQueries q;
     const uint32_t* norm_order;
+    const uint4* edge_meta;     // gather record of semantic[u][j] (n x degree)
+    const uint4* norm_meta;     // gather record of norm_order[i]
     uint32_t entry_count;
     const uint8_t* qflags;      // QF_VALID | QF_FALLBACK
     uint32_t vocab[2];          // per sparse path (learned, statistical): bitmap width, 0 = hash
