@@ -1,0 +1,208 @@
+// approx_score.cuh — warp-cooperative approximate hybrid scores (coalesced
+// row loads) used behind a certified error bound by the plain search
+// (search_plain.cu) and the NN-Descent pass (knn.cu).  The exact chains stay
+// in device_common.cuh.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace fgb {
+namespace approx {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr int kSG = 8;  // sparse rows in flight per warp round trip
+
+// One sparse query path staged in shared memory.  Vocabularies up to 64K
+// terms use a bitmap + rank structure (membership = one word test, value
+// index = the word's prefix count + a popcount: branch-free); larger ones a
+// bit filter in front of an open-addressing hash (device_common.cuh).
+struct PathQ {
+    uint32_t on;     // path active for this query (weight != 0, query nnz > 0)
+    uint32_t vocab;  // > 0: bitmap mode over [0, vocab)
+    uint32_t wm1;    // bitmap words - 1
+    const uint32_t* bm;
+    const uint16_t* pre;
+    const float* qv;  // weighted values (fp32, as build_query_vector) in ascending term order
+    const uint32_t* keys;
+    const float* vals;
+    const uint32_t* filt;
+    uint32_t mask;
+};
+
+// The weighted query value of term t (found=false, 0 when absent).
+template <bool kBitmap>
+__device__ __forceinline__ float q_lookup_t(const PathQ& P, uint32_t t, bool& found) {
+    if constexpr (kBitmap) {
+        const uint32_t tw = min(t >> 5, P.wm1);
+        const uint32_t word = P.bm[tw];
+        const uint32_t pre = P.pre[tw];
+        found = t < P.vocab && ((word >> (t & 31)) & 1u);
+        const float q = P.qv[pre + __popc(word & ((1u << (t & 31)) - 1u))];
+        return found ? q : 0.0f;
+    } else {
+        found = false;
+        float q = 0.0f;
+        if (t != kPad && filter_hit(P.filt, 2 * P.mask + 1, t)) found = hash_find(P.keys, P.vals, P.mask, t, q);
+        return found ? q : 0.0f;
+    }
+}
+
+__device__ __forceinline__ float q_lookup(const PathQ& P, uint32_t t, bool& found) {
+    return P.vocab ? q_lookup_t<true>(P, t, found) : q_lookup_t<false>(P, t, found);
+}
+
+// ------------------------------------------------------------ scoring
+// Exact fp64 products of the query terms among 4 postings, summed in fp64
+// (each product predicated on the lookup hit: no branches, no conversions
+// for misses).
+template <bool kBitmap>
+__device__ __forceinline__ double probe4(const uint4& ii, const float4& vv, const PathQ& P) {
+    bool f0, f1, f2, f3;
+    const float q0 = q_lookup_t<kBitmap>(P, ii.x, f0), q1 = q_lookup_t<kBitmap>(P, ii.y, f1);
+    const float q2 = q_lookup_t<kBitmap>(P, ii.z, f2), q3 = q_lookup_t<kBitmap>(P, ii.w, f3);
+    double s = 0.0;
+    if (f0) s = __fma_rn((double)q0, (double)vv.x, s);
+    if (f1) s = __fma_rn((double)q1, (double)vv.y, s);
+    if (f2) s = __fma_rn((double)q2, (double)vv.z, s);
+    if (f3) s = __fma_rn((double)q3, (double)vv.w, s);
+    return s;
+}
+
+// Reduce-scatter of kSG per-lane partial sums: node k's total (over all 32
+// lanes) ends in lanes [4k, 4k + 4) (bit-identical there).  9 shuffles
+// instead of 8 full butterflies.
+__device__ __forceinline__ double reduce_scatter8(double (&x)[8], uint32_t lane) {
+    const bool b4 = (lane >> 4) & 1u, b3 = (lane >> 3) & 1u, b2 = (lane >> 2) & 1u;
+    double y[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? x[i] : x[i + 4];
+        y[i] = (b4 ? x[i + 4] : x[i]) + __shfl_xor_sync(kFull, send, 16);
+    }
+    double z[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? y[i] : y[i + 2];
+        z[i] = (b3 ? y[i + 2] : y[i]) + __shfl_xor_sync(kFull, send, 8);
+    }
+    double r = (b2 ? z[1] : z[0]) + __shfl_xor_sync(kFull, b2 ? z[0] : z[1], 4);
+    r += __shfl_xor_sync(kFull, r, 2);
+    r += __shfl_xor_sync(kFull, r, 1);
+    return r;
+}
+
+// Warp-cooperative approximate sparse dot of one path for the F nodes held
+// by lanes 0..F-1 ((off4, nnz) each); lane j receives node j's sum.  kSG
+// nodes' first 128 postings (idx + val, coalesced 512 B each) are in flight
+// per round trip; postings 128.. of longer rows follow in a rolled loop.
+template <bool kBitmap>
+__device__ __noinline__ double sparse_group(const uint32_t* idx, const float* val, const PathQ P, uint32_t off4,
+                                            uint32_t nnz, uint32_t lane, uint32_t F) {
+    double mine = 0.0;
+    const uint4* i4 = reinterpret_cast<const uint4*>(idx);
+    const float4* v4 = reinterpret_cast<const float4*>(val);
+#pragma unroll 1
+    for (uint32_t g = 0; g < F; g += kSG) {
+        uint4 ii[kSG];
+        float4 vv[kSG];
+#pragma unroll
+        for (int k = 0; k < kSG; ++k) {
+            const uint32_t j = g + k;
+            const uint32_t oj = __shfl_sync(kFull, off4, j & 31);
+            const uint32_t nj = __shfl_sync(kFull, nnz, j & 31);
+            if (j < F && 4 * lane < nj) {
+                ii[k] = __ldg(i4 + oj + lane);
+                vv[k] = __ldg(v4 + oj + lane);
+            } else {
+                ii[k] = make_uint4(kPad, kPad, kPad, kPad);
+                vv[k] = make_float4(0, 0, 0, 0);
+            }
+        }
+        double part[8];
+#pragma unroll
+        for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap>(ii[k], vv[k], P);
+        const double r = reduce_scatter8(part, lane);
+        const uint32_t k = lane - g;  // owner lane g + k takes node k's sum from lane 4k
+        const double got = __shfl_sync(kFull, r, (4 * k) & 31);
+        if (lane >= g && lane < g + kSG) mine = got;
+    }
+    // postings 128.. of long rows (none for nnz <= 128)
+    uint32_t lm = __ballot_sync(kFull, lane < F && nnz > 128);
+#pragma unroll 1
+    while (lm) {
+        const uint32_t j = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t oj = __shfl_sync(kFull, off4, j), nj = __shfl_sync(kFull, nnz, j);
+        double e = 0.0;
+        for (uint32_t base = 32; 4 * base < nj; base += 32)
+            if (4 * (base + lane) < nj) e += probe4<kBitmap>(__ldg(i4 + oj + base + lane), __ldg(v4 + oj + base + lane), P);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
+        if (lane == j) mine += e;
+    }
+    return mine;
+}
+
+template <int NQ4>
+__device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, uint32_t lane, float4 (&b)[NQ4]) {
+    const float4* row = reinterpret_cast<const float4*>(c.dense + static_cast<uint64_t>(node) * c.dstride);
+    const uint32_t n4 = c.dstride >> 2;
+#pragma unroll
+    for (int k = 0; k < NQ4; ++k) {
+        const uint32_t col = k * 32 + lane;
+        b[k] = col < n4 ? __ldg(row + col) : make_float4(0, 0, 0, 0);
+    }
+}
+
+// Warp-cooperative approximate dense dot (coalesced 512-B loads per warp
+// instruction) for every lane-held node in `mask`, two rows per round trip;
+// fp32 partials of 4 elements, accumulated in fp64.
+template <int NQ4>
+__device__ __forceinline__ double dense_group(const DevCorpus& c, const float* qd, uint32_t node, uint32_t lane,
+                                              uint32_t mask) {
+    double mine = 0.0;
+    const float4* q4 = reinterpret_cast<const float4*>(qd);
+    const uint32_t n4 = c.dstride >> 2;
+    uint32_t m = mask;
+#pragma unroll 1
+    while (m) {
+        const uint32_t j0 = __ffs(m) - 1;
+        m &= m - 1;
+        const bool two = m != 0;
+        const uint32_t j1 = two ? __ffs(m) - 1 : j0;
+        if (two) m &= m - 1;
+        const uint32_t n0 = __shfl_sync(kFull, node, j0), n1 = __shfl_sync(kFull, node, j1);
+        float4 ra[NQ4], rb[NQ4];
+        dense_load<NQ4>(c, n0, lane, ra);
+        dense_load<NQ4>(c, n1, lane, rb);  // (j1 == j0 when alone: an L1 hit, result unused)
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int k = 0; k < NQ4; ++k) {
+            const uint32_t col = k * 32 + lane;
+            if (col < n4) {
+                const float4 q = q4[col];
+                float pa = q.x * ra[k].x, pb = q.x * rb[k].x;
+                pa = __fmaf_rn(q.y, ra[k].y, pa);
+                pb = __fmaf_rn(q.y, rb[k].y, pb);
+                pa = __fmaf_rn(q.z, ra[k].z, pa);
+                pb = __fmaf_rn(q.z, rb[k].z, pb);
+                pa = __fmaf_rn(q.w, ra[k].w, pa);
+                pb = __fmaf_rn(q.w, rb[k].w, pb);
+                sa += (double)pa;
+                sb += (double)pb;
+            }
+        }
+        // reduce-scatter of the pair: lanes 0-15 end with a's sum, 16-31 with b's
+        const bool hi = lane >= 16;
+        double r = (hi ? sb : sa) + __shfl_xor_sync(kFull, hi ? sa : sb, 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
+        const double ga = __shfl_sync(kFull, r, 0), gb = __shfl_sync(kFull, r, 16);
+        if (lane == j0) mine = ga;
+        if (two && lane == j1) mine = gb;
+    }
+    return mine;
+}
+
+}  // namespace approx
+}  // namespace fgb

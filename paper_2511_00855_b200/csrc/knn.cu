@@ -15,9 +15,12 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
+#include "approx_score.cuh"
 #include "fg_cuda.hpp"
 #include "knn.cuh"
 #include "stage_doc.cuh"
@@ -117,6 +120,9 @@ struct PassArgs {
     uint32_t pool_cap;  // power of two
     uint32_t lcap, scap;
     uint64_t lo;        // first node of this launch (vertex-range sharding)
+    // certified screening (NQ4 > 0): |approx - exact| <= eps32 * |u_d| * max_dnorm
+    // + eps64 * |u| * max_norm (search_plain.cu's bound with unit weights)
+    double eps32, eps64, max_dnorm, max_norm;
 };
 
 __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uint32_t mask,
@@ -130,7 +136,12 @@ __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uin
     if (fresh) atomicOr(&fbits[s >> 5], 1u << (s & 31));
 }
 
-// One NN-Descent pass for node u = lo + blockIdx.x.
+// One NN-Descent pass for node u = lo + blockIdx.x.  NQ4 > 0: candidates
+// are scored warp-cooperatively (coalesced rows, approx_score.cuh) and
+// rejected when certified worse than the running k-th entry; only the rest
+// get the exact chain.  NQ4 == 0 (dense rows > 1,024 floats): exact chains,
+// thread per candidate.
+template <int NQ4>
 __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
@@ -149,7 +160,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     uint32_t* S_id = T2_id + k;
     uint8_t* T_new = reinterpret_cast<uint8_t*>(S_id + nt);
     uint8_t* T2_new = T_new + k;
-    __shared__ uint32_t S_cnt;
+    // exactness of the stored scores (1: the reference's exact value, 0: the
+    // certified approximation +- eps) and resolution marks
+    uint8_t* T_ex = T2_new + k;
+    uint8_t* T2_ex = T_ex + k;
+    uint8_t* S_ex = T2_ex + k;
+    uint8_t* T_mk = S_ex + nt;
+    uint8_t* S_mk = T_mk + k;
+    __shared__ uint32_t S_cnt, n_mark;
     const uint32_t mask = a.pool_cap - 1;
 
     for (uint32_t j = tid; j < a.pool_cap; j += nt) keys[j] = kEmpty;
@@ -161,6 +179,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         T_id[j] = a.L_ids[u * k + j];
         T_sc[j] = a.L_sc[u * k + j];
         T_new[j] = 0;
+        T_ex[j] = 1;
     }
     if (tid == 0) S_cnt = 0;
     stage_doc(a.c, u, smem, a.lcap, a.scap, tid, nt, sq, [] { __syncthreads(); });
@@ -212,25 +231,119 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
 
     // Score fresh, new candidates; merge survivors into the running top-k.
     const double unorm = a.c.dnorm[u];
+    // u's dense row in fp32 (approximate path), after the flag arrays
+    float* qd = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(S_mk + nt) + 15) & ~uintptr_t(15));
+    approx::PathQ P[2];
+    double eps = 0.0;
+    if constexpr (NQ4 > 0) {
+        for (uint32_t j = tid; j < a.c.dstride; j += nt) qd[j] = a.c.dense[u * a.c.dstride + j];
+        for (int p = 0; p < 2; ++p) {
+            P[p].on = p == 0 ? sq.lmask != 0 : sq.smask != 0;
+            P[p].vocab = 0;  // hash lookups on the staged row
+            P[p].keys = p == 0 ? sq.lkeys : sq.skeys;
+            P[p].vals = p == 0 ? sq.lvals : sq.svals;
+            P[p].filt = p == 0 ? sq.lfilt : sq.sfilt;
+            P[p].mask = p == 0 ? sq.lmask : sq.smask;
+        }
+        eps = a.eps32 * unorm * (1.0 + 1e-10) * a.max_dnorm +
+              a.eps64 * sqrt(a.c.sqnorm[u]) * (1.0 + 1e-10) * a.max_norm + 1e-300;
+        __syncthreads();
+    }
+    const uint32_t lane = tid & 31;
+    // two stored scores decide their order (both exact, or apart by more than
+    // both error bounds; 1.25x margin for the subtraction's own rounding)
+    auto certain = [&](double va, uint8_t ea, double vb, uint8_t eb) {
+        return (ea && eb) || fabs(va - vb) > 1.25 * ((ea ? 0.0 : eps) + (eb ? 0.0 : eps));
+    };
     for (uint32_t base = 0; base < a.pool_cap; base += nt) {
         const uint32_t s = base + tid;
         const uint32_t id = s < a.pool_cap ? keys[s] : kEmpty;
         const bool cand = id != kEmpty && ((fbits[s >> 5] >> (s & 31)) & 1u) &&
                           !((hbits[s >> 5] >> (s & 31)) & 1u);
-        double sc;
-        // screened: candidates whose exact-score upper bound (sparse parts +
-        // |u||v|) is below the running k-th score never read their dense row
-        if (cand && hybrid_score_screened(a.c, sq, id, unorm, T_sc[k - 1], sc)) {
-            if (better(sc, id, T_sc[k - 1], T_id[k - 1])) {
-                const uint32_t slot = atomicAdd(&S_cnt, 1u);
-                S_sc[slot] = sc;
-                S_id[slot] = id;
+        const double tau = T_sc[k - 1];
+        const uint32_t tau_id = T_id[k - 1];
+        if constexpr (NQ4 > 0) {
+            // the k-th entry's value is exact or within eps: a candidate whose
+            // approximation is below it by more than both bounds never enters
+            const double tau_lo = tau - (T_ex[k - 1] ? 0.0 : eps);
+            const uint32_t fm = __ballot_sync(approx::kFull, cand);
+            if (fm) {  // warp-uniform
+                const uint32_t F = __popc(fm);
+                const uint32_t src = __fns(fm, 0, lane + 1);
+                const uint32_t cn = __shfl_sync(approx::kFull, id, src < 32 ? src : 0);
+                const bool mine = lane < F;
+                const uint4 mt = mine ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
+                double L = 0.0, S = 0.0;
+                if (P[0].on) L = approx::sparse_group<false>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
+                if (P[1].on) S = approx::sparse_group<false>(a.c.s_idx, a.c.s_val, P[1], mt.y, mt.z >> 16, lane, F);
+                // screening: the exact score is <= the bound (+ the approximation error)
+                bool keep = mine && !(score_upper_bound(unorm, (double)__uint_as_float(mt.w), L, S) + 2.0 * eps < tau_lo);
+                const uint32_t km = __ballot_sync(approx::kFull, keep);
+                const double D = approx::dense_group<NQ4>(a.c, qd, cn, lane, km);
+                const double v = __dadd_rn(__dadd_rn(D, L), S);
+                if (keep && !(v + eps < tau_lo)) {  // may enter: kept with its approximation
+                    const uint32_t slot = atomicAdd(&S_cnt, 1u);
+                    S_sc[slot] = v;
+                    S_id[slot] = cn;
+                    S_ex[slot] = 0;
+                }
+            }
+        } else {
+            double sc;
+            // screened: candidates whose exact-score upper bound (sparse parts +
+            // |u||v|) is below the running k-th score never read their dense row
+            if (cand && hybrid_score_screened(a.c, sq, id, unorm, tau, sc)) {
+                if (better(sc, id, tau, tau_id)) {
+                    const uint32_t slot = atomicAdd(&S_cnt, 1u);
+                    S_sc[slot] = sc;
+                    S_id[slot] = id;
+                    S_ex[slot] = 1;
+                }
             }
         }
         __syncthreads();
         const uint32_t m = S_cnt;
         __syncthreads();  // everyone holds m before S_cnt can change again
         if (m == 0) continue;
+        if constexpr (NQ4 > 0) {
+            // certify every comparison the rank-merge makes (S x T, S x S);
+            // uncertain entries get the reference's exact score, until none is
+            while (true) {
+                for (uint32_t i = tid; i < m; i += nt) S_mk[i] = 0;
+                for (uint32_t i = tid; i < k; i += nt) T_mk[i] = 0;
+                if (tid == 0) n_mark = 0;
+                __syncthreads();
+                for (uint32_t i = tid; i < m; i += nt) {
+                    bool mk = false;
+                    for (uint32_t q = 0; q < k; ++q)
+                        if (!certain(S_sc[i], S_ex[i], T_sc[q], T_ex[q])) {
+                            mk = true;
+                            if (!T_ex[q]) T_mk[q] = 1;
+                        }
+                    for (uint32_t q = 0; q < m; ++q)
+                        if (q != i && !certain(S_sc[i], S_ex[i], S_sc[q], S_ex[q])) mk = true;
+                    if (mk && !S_ex[i]) {
+                        S_mk[i] = 1;
+                        atomicAdd(&n_mark, 1u);
+                    }
+                }
+                __syncthreads();
+                uint32_t tm = 0;
+                for (uint32_t i = 0; i < k; ++i) tm += T_mk[i];
+                if (n_mark == 0 && tm == 0) break;
+                for (uint32_t i = tid; i < m; i += nt)
+                    if (S_mk[i]) {
+                        S_sc[i] = hybrid_score<2>(a.c, sq, S_id[i]);
+                        S_ex[i] = 1;
+                    }
+                for (uint32_t i = tid; i < k; i += nt)
+                    if (T_mk[i]) {
+                        T_sc[i] = hybrid_score<2>(a.c, sq, T_id[i]);
+                        T_ex[i] = 1;
+                    }
+                __syncthreads();
+            }
+        }
         // rank-merge T (sorted) with S (unsorted); ids are pairwise distinct
         for (uint32_t i = tid; i < k; i += nt) {
             uint32_t pos = i;
@@ -239,6 +352,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 T2_sc[pos] = T_sc[i];
                 T2_id[pos] = T_id[i];
                 T2_new[pos] = T_new[i];
+                T2_ex[pos] = T_ex[i];
             }
         }
         for (uint32_t i = tid; i < m; i += nt) {
@@ -257,6 +371,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 T2_sc[pos] = S_sc[i];
                 T2_id[pos] = S_id[i];
                 T2_new[pos] = 1;
+                T2_ex[pos] = S_ex[i];
             }
         }
         __syncthreads();
@@ -264,10 +379,19 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
             T_sc[i] = T2_sc[i];
             T_id[i] = T2_id[i];
             T_new[i] = T2_new[i];
+            T_ex[i] = T2_ex[i];
         }
         if (tid == 0) S_cnt = 0;
         __syncthreads();
     }
+    // the list's entries that carry approximations get their exact scores
+    // (the order among them was certified, so it is the exact order)
+    for (uint32_t i = tid; i < k; i += nt)
+        if (!T_ex[i]) {
+            T_sc[i] = hybrid_score<2>(a.c, sq, T_id[i]);
+            T_ex[i] = 1;
+        }
+    __syncthreads();
 
     uint32_t mine = 0;
     for (uint32_t i = tid; i < k; i += nt) {
@@ -283,8 +407,24 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
 size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap) {
     size_t b = (doc_stage_bytes(dstride, lcap, scap) + 15) & ~size_t(15);
     b += static_cast<size_t>(pool_cap) * 4 + 2 * (pool_cap / 32) * 4;
-    b += (2 * k + kPassThreads) * 8 + (2 * k + kPassThreads) * 4 + 2 * k;
+    b += (2 * k + kPassThreads) * 8 + (2 * k + kPassThreads) * 4;
+    b += 2 * k + 3 * k + 2 * kPassThreads + 16;          // new / exact / mark flags, alignment
+    b += static_cast<size_t>(dstride) * 4;                // fp32 dense row of u
     return b;
+}
+
+int pass_nq4(uint32_t dstride) {
+    const uint32_t need = ((dstride >> 2) + 31) / 32;
+    for (int v : {1, 2, 3, 4, 6, 8})
+        if (static_cast<uint32_t>(v) >= need) return v;
+    return 0;
+}
+
+template <int NQ4>
+void launch_pass(const PassArgs& a, uint64_t blocks, size_t sm, cudaStream_t s) {
+    FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel<NQ4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    knn_pass_kernel<NQ4><<<(unsigned)blocks, kPassThreads, sm, s>>>(a);
+    FGB_LAUNCH("knn_pass_kernel");
 }
 
 uint32_t pool_capacity(uint64_t n, uint32_t k) {
@@ -386,14 +526,33 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     const uint32_t lcap = hash_capacity(c.max_lnnz), scap = hash_capacity(c.max_snnz);
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
-               next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo};
+               next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo,
+               0.0, 0.0, 0.0, 0.0};
+    // error bound of the approximate pair scores (search_plain's, unit weights)
+    const double N = double(c.dstride) + c.max_lnnz + c.max_snnz + 2;
+    const double M = (c.dstride >> 2) + 2.0 * ((std::max(c.max_lnnz, c.max_snnz) + 127) / 128) + 16;
+    const double u32 = std::ldexp(1.0, -24), u64 = std::ldexp(1.0, -53);
+    a.eps32 = 4.0 * u32 / (1.0 - 4.0 * u32) * 1.01 + 1e-30;
+    a.eps64 = (N + M + 8) * u64 * 1.01;
+    a.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
+    a.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
     const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap);
     if (sm > 227 * 1024)
         throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
                                             std::to_string(sm) + " B)");
-    FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    knn_pass_kernel<<<(unsigned)(hi - lo), kPassThreads, sm, s>>>(a);
-    FGB_LAUNCH("knn_pass_kernel");
+    int nq4 = c.dc.meta ? pass_nq4(c.dstride) : 0;
+    if (const char* e = std::getenv("FGB_KNN_EXACT"))  // dev: the exact-chain-only pass
+        if (e[0] == '1') nq4 = 0;
+    const uint64_t blocks = hi - lo;
+    switch (nq4) {
+        case 1: launch_pass<1>(a, blocks, sm, s); break;
+        case 2: launch_pass<2>(a, blocks, sm, s); break;
+        case 3: launch_pass<3>(a, blocks, sm, s); break;
+        case 4: launch_pass<4>(a, blocks, sm, s); break;
+        case 6: launch_pass<6>(a, blocks, sm, s); break;
+        case 8: launch_pass<8>(a, blocks, sm, s); break;
+        default: launch_pass<0>(a, blocks, sm, s); break;
+    }
 }
 
 uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
