@@ -123,6 +123,7 @@ struct PassArgs {
     // certified screening (NQ4 > 0): |approx - exact| <= eps32 * |u_d| * max_dnorm
     // + eps64 * |u| * max_norm (search_plain.cu's bound with unit weights)
     double eps32, eps64, max_dnorm, max_norm;
+    uint32_t l_vocab;   // learned-path bitmap width (0: hash lookups)
 };
 
 __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uint32_t mask,
@@ -245,6 +246,39 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
             P[p].filt = p == 0 ? sq.lfilt : sq.sfilt;
             P[p].mask = p == 0 ? sq.lmask : sq.smask;
         }
+        // learned path of u as a bitmap + rank structure (branch-free lookups)
+        if (a.l_vocab && P[0].on) {
+            const uint32_t W = (a.l_vocab + 31) / 32;
+            uint32_t* bm = reinterpret_cast<uint32_t*>(qd + a.c.dstride);
+            uint16_t* pre = reinterpret_cast<uint16_t*>(bm + ((W + 3) & ~3u));
+            float* qv = reinterpret_cast<float*>(pre + ((W + 7) & ~7u));
+            const uint64_t lo = a.c.l_off[u];
+            const uint32_t ln = a.c.l_nnz[u];
+            const uint32_t* ui = a.c.l_idx + lo;
+            for (uint32_t w = tid; w < W; w += nt) bm[w] = 0;
+            __syncthreads();
+            for (uint32_t j = tid; j < ln; j += nt) {
+                const uint32_t t = ui[j];
+                atomicOr(&bm[t >> 5], 1u << (t & 31));
+                qv[j] = a.c.l_val[lo + j];  // u's row is ascending: rank = position
+            }
+            for (uint32_t w = tid; w < W; w += nt) {  // #terms < 32 w (lower bound in the sorted row)
+                uint32_t b = 0, e = ln;
+                while (b < e) {
+                    const uint32_t mid = (b + e) >> 1;
+                    if (ui[mid] < 32 * w)
+                        b = mid + 1;
+                    else
+                        e = mid;
+                }
+                pre[w] = static_cast<uint16_t>(b);
+            }
+            P[0].vocab = a.l_vocab;
+            P[0].wm1 = W - 1;
+            P[0].bm = bm;
+            P[0].pre = pre;
+            P[0].qv = qv;
+        }
         eps = a.eps32 * unorm * (1.0 + 1e-10) * a.max_dnorm +
               a.eps64 * sqrt(a.c.sqnorm[u]) * (1.0 + 1e-10) * a.max_norm + 1e-300;
         __syncthreads();
@@ -274,7 +308,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 const bool mine = lane < F;
                 const uint4 mt = mine ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
                 double L = 0.0, S = 0.0;
-                if (P[0].on) L = approx::sparse_group<false>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
+                if (P[0].on)
+                    L = P[0].vocab ? approx::sparse_group<true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F)
+                                   : approx::sparse_group<false>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
                 if (P[1].on) S = approx::sparse_group<false>(a.c.s_idx, a.c.s_val, P[1], mt.y, mt.z >> 16, lane, F);
                 // screening: the exact score is <= the bound (+ the approximation error)
                 bool keep = mine && !(score_upper_bound(unorm, (double)__uint_as_float(mt.w), L, S) + 2.0 * eps < tau_lo);
@@ -404,12 +440,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     if ((tid & 31) == 0 && mine) atomicAdd(a.changed, (unsigned long long)mine);
 }
 
-size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap) {
+size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap,
+                 uint32_t l_vocab) {
     size_t b = (doc_stage_bytes(dstride, lcap, scap) + 15) & ~size_t(15);
     b += static_cast<size_t>(pool_cap) * 4 + 2 * (pool_cap / 32) * 4;
     b += (2 * k + kPassThreads) * 8 + (2 * k + kPassThreads) * 4;
     b += 2 * k + 3 * k + 2 * kPassThreads + 16;          // new / exact / mark flags, alignment
     b += static_cast<size_t>(dstride) * 4;                // fp32 dense row of u
+    if (l_vocab) {                                        // u's learned bitmap, prefix, values
+        const size_t W = (l_vocab + 31) / 32;
+        b += ((W + 3) & ~size_t(3)) * 4 + ((W + 7) & ~size_t(7)) * 2 + static_cast<size_t>(lcap) * 4;
+    }
     return b;
 }
 
@@ -527,7 +568,7 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0};
+               0.0, 0.0, 0.0, 0.0, 0};
     // error bound of the approximate pair scores (search_plain's, unit weights)
     const double N = double(c.dstride) + c.max_lnnz + c.max_snnz + 2;
     const double M = (c.dstride >> 2) + 2.0 * ((std::max(c.max_lnnz, c.max_snnz) + 127) / 128) + 16;
@@ -536,7 +577,9 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     a.eps64 = (N + M + 8) * u64 * 1.01;
     a.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
     a.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
-    const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap);
+    a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;
+    if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab) > 227 * 1024) a.l_vocab = 0;
+    const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab);
     if (sm > 227 * 1024)
         throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
                                             std::to_string(sm) + " B)");
