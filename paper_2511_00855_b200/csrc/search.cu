@@ -1209,7 +1209,9 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
             pl.eps_scale = 1.0;
             if (const char* e = std::getenv("FGB_EPS_SCALE")) pl.eps_scale = std::atof(e);
-            pl.prefetch = 0;  // tools/ubench_latency.cu: bulk L2 prefetch slows the demand loads
+            // bulk L2 prefetch of the screened survivors' dense rows (1); prefetching
+            // every first-time neighbour's row (2) slowed demand loads (tools/ubench_latency.cu)
+            pl.prefetch = 1;
             if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) pl.prefetch = std::atoi(e);
             if (plain_warp_smem(pl) > 0) {
                 const uint64_t slots = plain_slots(pl, nq, c.device);
