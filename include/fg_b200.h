@@ -313,6 +313,15 @@ int fg_index_export(const fg_index* ix, uint32_t* semantic, uint64_t* keyword_pt
 int fg_index_build_times(const fg_index* ix, double* seconds5);
 int fg_index_free(fg_index* ix);
 
+/* The reference's binary index file HYBGRIX1 v1 (io.hpp:63-71, io.cpp:242-671,
+ * SURVEY 8(f2)).  fg_index_serialize writes exactly the bytes
+ * fusegraph::serialize_index writes for the same index (the reference's
+ * deserialize_index, CLI `query`/`bench` load it); fg_index_deserialize loads
+ * a reference-written file into a new device corpus + index (errors:
+ * not-an-index, version-mismatch, truncated-file, checksum-failure, io-error). */
+int fg_index_serialize(const fg_index* ix, const char* path, uint64_t* bytes);
+int fg_index_deserialize(const char* path, int device, fg_corpus** corpus, fg_index** index);
+
 /* ------------------------------------------------------------------------ */
 /* Multi-GPU construction: vertex-range sharding              */
 /* ------------------------------------------------------------------------ */

@@ -68,6 +68,8 @@ class _Base:
             "index_export": (C.c_int, [C.c_void_p, A.u32p, A.u64p, A.u32p, A.u64p, A.u32p,
                                        A.u32p]),
             "index_set_deleted": (C.c_int, [C.c_void_p, A.u8p]),
+            "index_serialize": (C.c_int, [C.c_void_p, C.c_char_p, A.u64p]),
+            "index_deserialize": (C.c_int, [C.c_char_p, P(C.c_void_p)]),
             "batch_query": (C.c_int, [C.c_void_p, P(A.QueryView), P(A.SearchOpts), C.c_uint,
                                       P(A.SearchResults)]),
             "brute_force": (C.c_int, [C.c_void_p, P(A.QueryView), C.c_uint, P(A.SearchResults)]),
@@ -193,6 +195,16 @@ class _Base:
         p = A.BuildParams(degree, knn_k, knn_iterations, seed, logical_cap, default_entity_hops,
                           int(per_neighbour))
         self._check(self._index_build(store.h, C.byref(p), threads, C.byref(h)))
+        return _Handle(h, self._index_free)
+
+    def index_serialize(self, ix, path: str) -> int:
+        nb = C.c_uint64()
+        self._check(self._index_serialize(ix.h, path.encode(), C.byref(nb)))
+        return nb.value
+
+    def index_deserialize(self, path: str):
+        h = C.c_void_p()
+        self._check(self._index_deserialize(path.encode(), C.byref(h)))
         return _Handle(h, self._index_free)
 
     def index_create(self, store, graph: dict, knn_k=0):

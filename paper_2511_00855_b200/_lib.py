@@ -64,6 +64,8 @@ def _declare(lib):
         "fg_index_export": (C.c_int, [C.c_void_p, A.u32p, A.u64p, A.u32p, A.u64p, A.u32p,
                                       A.u32p]),
         "fg_index_build_times": (C.c_int, [C.c_void_p, A.f64p]),
+        "fg_index_serialize": (C.c_int, [C.c_void_p, C.c_char_p, A.u64p]),
+        "fg_index_deserialize": (C.c_int, [C.c_char_p, C.c_int, P(C.c_void_p), P(C.c_void_p)]),
         "fg_comm_unique_id": (C.c_int, [A.u8p]),
         "fg_comm_init": (C.c_int, [C.c_int, C.c_int, A.u8p, C.c_int, P(C.c_void_p)]),
         "fg_comm_free": (C.c_int, [C.c_void_p]),

@@ -200,6 +200,8 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
         c->n = v->n;
         c->dim = v->dense_dim;
         c->dstride = round4(std::max<uint32_t>(v->dense_dim, 1));
+        c->learned_dim = v->learned_dim;
+        c->statistical_dim = v->statistical_dim;
         FGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         cudaStream_t s = c->stream;
         const uint64_t n = v->n;

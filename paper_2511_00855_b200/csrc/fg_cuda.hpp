@@ -112,6 +112,7 @@ struct fg_corpus {
     uint32_t max_lnnz = 0, max_snnz = 0;
     uint64_t l_nnz_total4 = 0, s_nnz_total4 = 0;  // padded posting counts / 4
     uint32_t l_vocab = 0, s_vocab = 0;             // 1 + the largest term id per path
+    uint32_t learned_dim = 0, statistical_dim = 0; // DocumentStore vocabulary bounds (types.hpp:121-122)
     fgb::DevCorpus dc{};
     fgb::DevBuf<float> dense, l_val, s_val;
     fgb::DevBuf<uint64_t> l_off, s_off, kw_ptr, ent_ptr;

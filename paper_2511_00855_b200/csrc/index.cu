@@ -3,6 +3,7 @@
 // host: entity map and logical edges (logical.cpp:9-68), KG adjacency
 // (types.cpp:29-45) and the norm order (index.cpp:12-23).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <numeric>
 #include <thread>
@@ -119,6 +120,17 @@ void index_finish(fg_index& ix, const fg_kg_view* kgv) {
         for (const uint32_t* e = c.entities.begin(u); e != c.entities.end(u); ++e)
             ix.entity_map[*e].push_back(static_cast<uint32_t>(u));
 
+    // KnowledgeGraph triplets as the reference keeps them (types.cpp:29-40:
+    // sorted by (source, relation, target), duplicates removed)
+    {
+        std::vector<std::array<uint32_t, 3>> t;
+        if (kgv)
+            for (uint64_t i = 0; i < kgv->count; ++i) t.push_back({kgv->source[i], kgv->relation[i], kgv->target[i]});
+        std::sort(t.begin(), t.end());
+        t.erase(std::unique(t.begin(), t.end()), t.end());
+        ix.triplets.clear();
+        for (const auto& x : t) ix.triplets.insert(ix.triplets.end(), x.begin(), x.end());
+    }
     // logical edges, unless given
     const HostKg kg = make_kg(kgv);
     if (ix.lg_ptr_h.empty()) {

@@ -34,6 +34,7 @@ struct fg_index {
     std::vector<uint32_t> lg_h;  // 4 per edge
     std::vector<uint32_t> norm_order_h;
     std::map<uint32_t, std::vector<uint32_t>> entity_map;  // EntityMap (logical.hpp:21)
+    std::vector<uint32_t> triplets;  // KnowledgeGraph::triplets(): (s, r, t) sorted, unique
     uint32_t max_kw_edges = 0, max_logical_group = 0;
     double build_seconds[5] = {0, 0, 0, 0, 0};
 

@@ -195,6 +195,24 @@ class HybridIndex:
         return dict(degree=deg.value, semantic=sem, keyword=A.CSR(kp, ki), logical_ptr=lp,
                     logical=lg, norm_order=no)
 
+    def serialize(self, path: str) -> int:
+        """serialize_index (io.hpp:63): HYBGRIX1 v1, the reference's bytes."""
+        nb = C.c_uint64()
+        check(lib().fg_index_serialize(self.h, path.encode(), C.byref(nb)))
+        return nb.value
+
+    @staticmethod
+    def deserialize(path: str, device: int = 0) -> "HybridIndex":
+        """deserialize_index (io.hpp:71) into HBM; the index owns its corpus."""
+        ch, ih = C.c_void_p(), C.c_void_p()
+        check(lib().fg_index_deserialize(path.encode(), device, C.byref(ch), C.byref(ih)))
+        dc = DeviceCorpus.__new__(DeviceCorpus)
+        dc.h, dc.device, dc.host = ch, device, None
+        n, d = C.c_uint64(), C.c_uint32()
+        check(lib().fg_corpus_size(ch, C.byref(n), C.byref(d)))
+        dc.n, dc.dense_dim = n.value, d.value
+        return HybridIndex(dc, ih)
+
     def build_times(self) -> dict:
         t = np.zeros(5, np.float64)
         check(lib().fg_index_build_times(self.h, A.ptr(t, A.f64p)))
