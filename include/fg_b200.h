@@ -313,6 +313,22 @@ int fg_index_export(const fg_index* ix, uint32_t* semantic, uint64_t* keyword_pt
 int fg_index_build_times(const fg_index* ix, double* seconds5);
 int fg_index_free(fg_index* ix);
 
+/* InsertParams (update.hpp:22-28). */
+typedef struct fg_insert_params {
+    uint32_t knn_k;                 /* candidate width; 0: the build's knn_k */
+    uint32_t nn_descent_iterations; /* batch-local NN-Descent passes (10) */
+    uint32_t threads;               /* accepted for API parity; the GPU ignores it */
+} fg_insert_params;
+
+/* insert_batch (update.hpp:33-34, update.cpp:33-197): appends `docs` to the
+ * index's corpus and links them exactly as the reference does (beam-search
+ * candidates over the current graph, NN-Descent among the batch, per-node
+ * refinery, batch-local reverse half, weakest-reverse-slot replacement on
+ * existing nodes, norm order rebuilt).  Validation happens first and leaves
+ * the index untouched on error (duplicate-id, dim-mismatch, nonfinite-value,
+ * unsorted-sparse, zero-sparse-value, invalid-k, corpus-too-small). */
+int fg_index_insert(fg_index* ix, const fg_corpus_view* docs, const fg_insert_params* params);
+
 /* The reference's binary index file HYBGRIX1 v1 (io.hpp:63-71, io.cpp:242-671,
  * SURVEY 8(f2)).  fg_index_serialize writes exactly the bytes
  * fusegraph::serialize_index writes for the same index (the reference's

@@ -30,6 +30,7 @@
 #include "fusegraph/rng.hpp"
 #include "fusegraph/scoring.hpp"
 #include "fusegraph/search.hpp"
+#include "fusegraph/update.hpp"
 #include "fusegraph/synth.hpp"
 #include "fusegraph/types.hpp"
 
@@ -545,6 +546,26 @@ int fgref_index_deserialize(const char* path, fgref_index** out) {
         *out = ix.release();
     });
 }
+// insert_batch (update.hpp:33): documents built exactly as fgref_store_create
+// builds them (make_document), then the reference's own insertion.
+int fgref_index_insert(fgref_index* h, const fg_corpus_view* v, uint32_t knn_k, uint32_t iters) {
+    return guarded([&] {
+        std::vector<R::DocumentRecord> docs;
+        for (uint64_t i = 0; i < v->n; ++i) {
+            R::DenseVector d;
+            d.values.assign(v->dense + i * v->dense_dim, v->dense + (i + 1) * v->dense_dim);
+            std::optional<std::vector<uint32_t>> kw;
+            if (v->keywords.ptr) kw = list_row(v->keywords, i);
+            docs.push_back(R::make_document(v->doc_id ? v->doc_id[i] : i, std::move(d), sparse_row(v->learned, i),
+                                            sparse_row(v->statistical, i), kw, list_row(v->entities, i)));
+        }
+        R::InsertParams p;
+        p.knn_k = knn_k;
+        p.nn_descent_iterations = iters;
+        R::insert_batch(h->index, std::move(docs), p);
+    });
+}
+
 int fgref_index_validate(const fgref_index* h) {
     return guarded([&] { R::validate_index(h->index); });
 }

@@ -69,6 +69,7 @@ class _Base:
                                        A.u32p]),
             "index_set_deleted": (C.c_int, [C.c_void_p, A.u8p]),
             "index_serialize": (C.c_int, [C.c_void_p, C.c_char_p, A.u64p]),
+            "index_insert": (C.c_int, [C.c_void_p, P(A.CorpusView), C.c_uint32, C.c_uint32]),
             "index_deserialize": (C.c_int, [C.c_char_p, P(C.c_void_p)]),
             "batch_query": (C.c_int, [C.c_void_p, P(A.QueryView), P(A.SearchOpts), C.c_uint,
                                       P(A.SearchResults)]),
@@ -196,6 +197,10 @@ class _Base:
                           int(per_neighbour))
         self._check(self._index_build(store.h, C.byref(p), threads, C.byref(h)))
         return _Handle(h, self._index_free)
+
+    def index_insert(self, ix, docs: A.Corpus, knn_k=0, iterations=10):
+        v = docs.view()
+        self._check(self._index_insert(ix.h, C.byref(v), knn_k, iterations))
 
     def index_serialize(self, ix, path: str) -> int:
         nb = C.c_uint64()

@@ -193,6 +193,10 @@ def null_list():
     return ListView(C.cast(None, u64p), C.cast(None, u32p))
 
 
+class InsertParams(C.Structure):
+    _fields_ = [("knn_k", C.c_uint32), ("nn_descent_iterations", C.c_uint32), ("threads", C.c_uint32)]
+
+
 class Corpus:
     """DocumentStore (types.hpp:119-133) as structure-of-arrays."""
 

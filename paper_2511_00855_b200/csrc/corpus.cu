@@ -183,6 +183,148 @@ void QueryUpload::upload(const fg_query_view& q, cudaStream_t s) {
 }
 
 
+// Device-derived state of a corpus whose rows are uploaded: the DevCorpus
+// view, squared norms (finalize_fused, types.cpp:74-79), the packed gather
+// records, and the host copies / maxima the error bounds use.
+void corpus_finalize(fg_corpus& c) {
+    const uint64_t n = c.n;
+    cudaStream_t s = c.stream;
+    c.sqnorm.alloc(n);
+    c.dnorm.alloc(n);
+
+    c.dc = DevCorpus{n,
+              c.dim,
+              c.dstride,
+              c.dense.get(),
+              c.l_off.get(),
+              c.l_nnz.get(),
+              c.l_idx.get(),
+              c.l_val.get(),
+              c.s_off.get(),
+              c.s_nnz.get(),
+              c.s_idx.get(),
+              c.s_val.get(),
+              c.kw_ptr.get(),
+              c.kw_idx.get(),
+              c.ent_ptr.get(),
+              c.ent_idx.get(),
+              c.sqnorm.get(),
+              c.dnorm.get(),
+              c.deleted.get(),
+              nullptr};
+    sqnorm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c.dc, c.sqnorm.get(), c.dnorm.get());
+    FGB_LAUNCH("sqnorm_kernel");
+    // offsets / 4 must fit 32 bits and nnz 16 bits for the packed record
+    const uint64_t l_end = c.l_nnz_total4, s_end = c.s_nnz_total4;
+    if (c.max_lnnz < 65536 && c.max_snnz < 65536 && l_end < (1ull << 32) && s_end < (1ull << 32)) {
+        c.meta.alloc(n);
+        meta_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c.dc, c.dnorm.get(), c.meta.get());
+        FGB_LAUNCH("meta_kernel");
+        c.dc.meta = c.meta.get();
+    }
+    c.sqnorm_h.resize(n);
+    c.sqnorm.download(c.sqnorm_h.data(), n, s);
+    FGB_CUDA(cudaStreamSynchronize(s));
+    c.max_sqnorm = 0.0;
+    for (double x : c.sqnorm_h) c.max_sqnorm = std::max(c.max_sqnorm, x);
+    {
+        std::vector<double> dn(n);
+        c.dnorm.download(dn.data(), n, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        c.max_dnorm = 0.0;
+        for (double x : dn) c.max_dnorm = std::max(c.max_dnorm, x);
+    }
+}
+
+// Appends the rows of `v` to the device corpus (insert_batch, update.cpp:94-103):
+// device arrays are reallocated with the old rows copied device-to-device and
+// the new ones uploaded; keywords default to the statistical support as
+// make_document does (corpus.cpp:113-117).  Validation happens in the caller.
+void corpus_append(fg_corpus& c, const fg_corpus_view& v) {
+    const uint64_t n0 = c.n, b = v.n, n = n0 + b;
+    cudaStream_t s = c.stream;
+    {
+        DevBuf<float> dense(n * c.dstride);
+        FGB_CUDA(cudaMemcpyAsync(dense.get(), c.dense.get(), n0 * c.dstride * 4, cudaMemcpyDeviceToDevice, s));
+        std::vector<float> pad(b * c.dstride, 0.0f);
+        for (uint64_t i = 0; i < b; ++i) std::memcpy(pad.data() + i * c.dstride, v.dense + i * c.dim, c.dim * 4);
+        FGB_CUDA(cudaMemcpyAsync(dense.get() + n0 * c.dstride, pad.data(), pad.size() * 4, cudaMemcpyHostToDevice, s));
+        FGB_CUDA(cudaStreamSynchronize(s));
+        c.dense = std::move(dense);
+    }
+    for (int p = 0; p < 2; ++p) {
+        const bool learned = p == 0;
+        std::vector<uint64_t> off;
+        std::vector<uint32_t> nnz, idx;
+        std::vector<float> val;
+        uint32_t mx = 0;
+        build_sparse(learned ? v.learned : v.statistical, b, off, nnz, idx, val, mx,
+                     learned ? "learned" : "statistical");
+        uint64_t& total4 = learned ? c.l_nnz_total4 : c.s_nnz_total4;
+        const uint64_t base = total4 * 4, add = idx.size();
+        for (auto& o : off) o += base;
+        DevBuf<uint64_t>& doff = learned ? c.l_off : c.s_off;
+        DevBuf<uint32_t>& dnnz = learned ? c.l_nnz : c.s_nnz;
+        DevBuf<uint32_t>& didx = learned ? c.l_idx : c.s_idx;
+        DevBuf<float>& dval = learned ? c.l_val : c.s_val;
+        DevBuf<uint64_t> noff(n);
+        DevBuf<uint32_t> nnnz(n), nidx(std::max<uint64_t>(base + add, 4));
+        DevBuf<float> nval(std::max<uint64_t>(base + add, 4));
+        FGB_CUDA(cudaMemcpyAsync(noff.get(), doff.get(), n0 * 8, cudaMemcpyDeviceToDevice, s));
+        FGB_CUDA(cudaMemcpyAsync(nnnz.get(), dnnz.get(), n0 * 4, cudaMemcpyDeviceToDevice, s));
+        FGB_CUDA(cudaMemcpyAsync(noff.get() + n0, off.data(), b * 8, cudaMemcpyHostToDevice, s));
+        FGB_CUDA(cudaMemcpyAsync(nnnz.get() + n0, nnz.data(), b * 4, cudaMemcpyHostToDevice, s));
+        if (base) {
+            FGB_CUDA(cudaMemcpyAsync(nidx.get(), didx.get(), base * 4, cudaMemcpyDeviceToDevice, s));
+            FGB_CUDA(cudaMemcpyAsync(nval.get(), dval.get(), base * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        if (add) {
+            FGB_CUDA(cudaMemcpyAsync(nidx.get() + base, idx.data(), add * 4, cudaMemcpyHostToDevice, s));
+            FGB_CUDA(cudaMemcpyAsync(nval.get() + base, val.data(), add * 4, cudaMemcpyHostToDevice, s));
+        }
+        FGB_CUDA(cudaStreamSynchronize(s));
+        doff = std::move(noff);
+        dnnz = std::move(nnnz);
+        didx = std::move(nidx);
+        dval = std::move(nval);
+        total4 += add / 4;
+        (learned ? c.max_lnnz : c.max_snnz) = std::max(learned ? c.max_lnnz : c.max_snnz, mx);
+        uint32_t& voc = learned ? c.l_vocab : c.s_vocab;
+        for (uint32_t t : idx)
+            if (t != kPad) voc = std::max(voc, t + 1);
+    }
+    HostList kw, ents;
+    if (v.keywords.ptr) {
+        copy_list(v.keywords, b, kw);
+    } else {
+        kw.ptr.assign(b + 1, 0);
+        for (uint64_t i = 0; i < b; ++i) {
+            const uint64_t lo = v.statistical.ptr ? v.statistical.ptr[i] : 0;
+            const uint64_t hi = v.statistical.ptr ? v.statistical.ptr[i + 1] : 0;
+            kw.idx.insert(kw.idx.end(), v.statistical.idx + lo, v.statistical.idx + hi);
+            kw.ptr[i + 1] = kw.idx.size();
+        }
+    }
+    copy_list(v.entities, b, ents);
+    auto extend = [&](HostList& dst, const HostList& src) {
+        const uint64_t base = dst.ptr.back();
+        for (uint64_t i = 0; i < b; ++i) dst.ptr.push_back(base + src.ptr[i + 1]);
+        dst.idx.insert(dst.idx.end(), src.idx.begin(), src.idx.end());
+    };
+    extend(c.keywords, kw);
+    extend(c.entities, ents);
+    c.kw_ptr.upload(c.keywords.ptr, s);
+    c.kw_idx.upload(c.keywords.idx.empty() ? std::vector<uint32_t>(1, 0) : c.keywords.idx, s);
+    c.ent_ptr.upload(c.entities.ptr, s);
+    c.ent_idx.upload(c.entities.idx.empty() ? std::vector<uint32_t>(1, 0) : c.entities.idx, s);
+    for (uint64_t i = 0; i < b; ++i) c.doc_id.push_back(v.doc_id ? v.doc_id[i] : n0 + i);
+    c.deleted_h.resize(n, 0);
+    c.deleted.upload(c.deleted_h, s);
+    FGB_CUDA(cudaStreamSynchronize(s));
+    c.n = n;
+    corpus_finalize(c);
+}
+
 }  // namespace fgb
 
 using namespace fgb;
@@ -264,51 +406,7 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
         if (v->deleted)
             for (uint64_t i = 0; i < n; ++i) c->deleted_h[i] = v->deleted[i] ? 1 : 0;
         c->deleted.upload(c->deleted_h, s);
-        c->sqnorm.alloc(n);
-        c->dnorm.alloc(n);
-
-        c->dc = DevCorpus{n,
-                          c->dim,
-                          c->dstride,
-                          c->dense.get(),
-                          c->l_off.get(),
-                          c->l_nnz.get(),
-                          c->l_idx.get(),
-                          c->l_val.get(),
-                          c->s_off.get(),
-                          c->s_nnz.get(),
-                          c->s_idx.get(),
-                          c->s_val.get(),
-                          c->kw_ptr.get(),
-                          c->kw_idx.get(),
-                          c->ent_ptr.get(),
-                          c->ent_idx.get(),
-                          c->sqnorm.get(),
-                          c->dnorm.get(),
-                          c->deleted.get(),
-                          nullptr};
-        sqnorm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->sqnorm.get(), c->dnorm.get());
-        FGB_LAUNCH("sqnorm_kernel");
-        // offsets / 4 must fit 32 bits and nnz 16 bits for the packed record
-        const uint64_t l_end = c->l_nnz_total4, s_end = c->s_nnz_total4;
-        if (c->max_lnnz < 65536 && c->max_snnz < 65536 && l_end < (1ull << 32) && s_end < (1ull << 32)) {
-            c->meta.alloc(n);
-            meta_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->dc, c->dnorm.get(), c->meta.get());
-            FGB_LAUNCH("meta_kernel");
-            c->dc.meta = c->meta.get();
-        }
-        c->sqnorm_h.resize(n);
-        c->sqnorm.download(c->sqnorm_h.data(), n, s);
-        FGB_CUDA(cudaStreamSynchronize(s));
-        c->max_sqnorm = 0.0;
-        for (double x : c->sqnorm_h) c->max_sqnorm = std::max(c->max_sqnorm, x);
-        {
-            std::vector<double> dn(n);
-            c->dnorm.download(dn.data(), n, s);
-            FGB_CUDA(cudaStreamSynchronize(s));
-            c->max_dnorm = 0.0;
-            for (double x : dn) c->max_dnorm = std::max(c->max_dnorm, x);
-        }
+        corpus_finalize(*c);
         *out = c.release();
     });
 }

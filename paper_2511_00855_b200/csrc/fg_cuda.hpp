@@ -167,4 +167,9 @@ struct QueryUpload {
 
 inline uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
 
+// Derived device state of an uploaded corpus (norms, gather records, maxima).
+void corpus_finalize(fg_corpus& c);
+// Appends the rows of `v` (insert_batch); validation is the caller's.
+void corpus_append(fg_corpus& c, const fg_corpus_view& v);
+
 }  // namespace fgb

@@ -3,6 +3,10 @@
 // host: entity map and logical edges (logical.cpp:9-68), KG adjacency
 // (types.cpp:29-45) and the norm order (index.cpp:12-23).
 #include <algorithm>
+#include <memory>
+#include <cmath>
+#include <unordered_set>
+#include <unordered_map>
 #include <array>
 #include <chrono>
 #include <numeric>
@@ -216,11 +220,329 @@ void index_finish(fg_index& ix, const fg_kg_view* kgv) {
     }
 }
 
+
+// ---------------------------------------------------------------- insert_batch
+// insert_batch (update.cpp:33-197) on the device index.  Candidate sources:
+// (a) the batched beam search of each new doc over the current index (unit
+// weights, k = kk, beam 2kk; search.cpp), (b) NN-Descent among the batch
+// (knn.cu) seeded mix_seed(build_seed, n_old); then the per-node refinery
+// (refine_node_kernel) over the merged candidates, the batch-local reverse
+// half, keyword recycling and logical edges for the new nodes, and the
+// deterministic weakest-reverse-slot replacement on existing nodes (host loop
+// over exact GPU pair scores), the norm order rebuilt.
+namespace {
+
+struct Cand {
+    uint32_t id;
+    double score;
+};
+
+void check_sparse(const fg_sparse_view& sv, uint64_t i, const std::string& where, const char* path) {
+    if (!sv.ptr) return;
+    for (uint64_t j = sv.ptr[i]; j < sv.ptr[i + 1]; ++j) {
+        if (j > sv.ptr[i] && sv.idx[j] <= sv.idx[j - 1])
+            throw Error("unsorted-sparse", where + ": " + path + " indices must be strictly ascending");
+        if (!std::isfinite(sv.val[j]))
+            throw Error("nonfinite-value", where + ": " + path + " holds a non-finite value");
+        if (sv.val[j] == 0.0f)
+            throw Error("zero-sparse-value", where + ": " + path + " stores an explicit zero at index " +
+                                                 std::to_string(sv.idx[j]));
+    }
+}
+
+void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert_params& p) {
+    fg_corpus& c = *ix.corpus;
+    cudaStream_t s = c.stream;
+    const uint64_t n_old = c.n, batch = in.n;
+    const uint32_t d = ix.degree;
+    const uint32_t kk = p.knn_k ? p.knn_k : ix.knn_k;
+    if (batch == 0) return;
+    if (kk < d) throw Error("invalid-k", "insert candidate width must be at least the degree");
+
+    // ---- validate before touching anything (update.cpp:43-63)
+    std::unordered_set<uint64_t> ids(c.doc_id.begin(), c.doc_id.end());
+    std::vector<uint64_t> doc_id(batch);
+    for (uint64_t i = 0; i < batch; ++i) {
+        doc_id[i] = in.doc_id ? in.doc_id[i] : n_old + i;
+        const std::string where = "doc " + std::to_string(doc_id[i]);
+        if (ids.count(doc_id[i])) throw Error("duplicate-id", where + ": id already in the index");
+        if (in.dense_dim != c.dim)
+            throw Error("dim-mismatch", where + ": dense dimension " + std::to_string(in.dense_dim) +
+                                            " differs from corpus " + std::to_string(c.dim));
+        for (uint32_t j = 0; j < in.dense_dim; ++j)
+            if (!std::isfinite(in.dense[i * in.dense_dim + j]))
+                throw Error("nonfinite-value", where + ": dense holds a non-finite value");
+        check_sparse(in.learned, i, where, "learned");
+        check_sparse(in.statistical, i, where, "statistical");
+    }
+    for (uint64_t i = 1; i < batch; ++i)
+        for (uint64_t j = 0; j < i; ++j)
+            if (doc_id[i] == doc_id[j])
+                throw Error("duplicate-id", "doc " + std::to_string(doc_id[i]) + ": id repeated within the batch");
+    // keywords / entities sorted unique (update.cpp:58-59), keywords default to
+    // the statistical support (make_document, corpus.cpp:113-117)
+    auto sorted_unique = [&](const fg_list_view& lv, bool kw) {
+        HostList out;
+        for (uint64_t i = 0; i < batch; ++i) {
+            std::vector<uint32_t> row;
+            if (lv.ptr)
+                row.assign(lv.idx + lv.ptr[i], lv.idx + lv.ptr[i + 1]);
+            else if (kw && in.statistical.ptr)
+                row.assign(in.statistical.idx + in.statistical.ptr[i], in.statistical.idx + in.statistical.ptr[i + 1]);
+            std::sort(row.begin(), row.end());
+            row.erase(std::unique(row.begin(), row.end()), row.end());
+            out.idx.insert(out.idx.end(), row.begin(), row.end());
+            out.ptr.push_back(out.idx.size());
+        }
+        return out;
+    };
+    const HostList kws = sorted_unique(in.keywords, true), ents = sorted_unique(in.entities, false);
+    fg_corpus_view v = in;
+    v.doc_id = doc_id.data();
+    v.deleted = nullptr;
+    v.keywords = fg_list_view{kws.ptr.data(), kws.idx.data()};
+    v.entities = fg_list_view{ents.ptr.data(), ents.idx.data()};
+
+    // ---- (a) nearest existing nodes through the current graph (update.cpp:18-29)
+    std::vector<std::vector<Cand>> from_index(batch), from_batch(batch);
+    {
+        std::vector<fg_weights> w(batch, fg_weights{1.f, 1.f, 1.f, 0.f});
+        std::vector<uint32_t> kq(batch, kk), bq(batch, 2 * kk);
+        fg_query_view q{};
+        q.count = batch;
+        q.dense_dim = in.dense_dim;
+        q.dense = in.dense;
+        q.learned = in.learned;
+        q.statistical = in.statistical;
+        q.weights = w.data();
+        q.k = kq.data();
+        q.beam_width = bq.data();
+        std::vector<uint64_t> rd(batch * kk);
+        std::vector<uint32_t> rn(batch * kk), rc(batch);
+        std::vector<double> rs(batch * kk);
+        std::vector<char> errs(batch * 256);
+        fg_search_results r{};
+        r.hit_stride = kk;
+        r.doc_id = rd.data();
+        r.node = rn.data();
+        r.score = rs.data();
+        r.hit_count = rc.data();
+        r.errors = errs.data();
+        r.error_stride = 256;
+        fg_search_opts o{32, 1};  // SearchOptions{} (kDefaultEntryCount, index.hpp:55)
+        if (fg_batch_query(&ix, &q, &o, &r) != FG_OK) throw Error(fg_last_error_code(), fg_last_error_message());
+        for (uint64_t i = 0; i < batch; ++i) {
+            if (errs[i * 256]) {
+                const std::string e(&errs[i * 256]);
+                throw Error(e.substr(0, e.find(':')), e);
+            }
+            for (uint32_t j = 0; j < rc[i]; ++j) from_index[i].push_back({rn[i * kk + j], rs[i * kk + j]});
+        }
+    }
+    // ---- (b) neighbour-descent among the batch itself (update.cpp:71-88)
+    if (batch > 1) {
+        fg_corpus* tmp = nullptr;
+        if (fg_corpus_upload(&v, c.device, &tmp) != FG_OK) throw Error(fg_last_error_code(), fg_last_error_message());
+        std::unique_ptr<fg_corpus, int (*)(fg_corpus*)> tg(tmp, fg_corpus_free);
+        DevKnn g;
+        const uint32_t kb = std::min<uint32_t>(kk, static_cast<uint32_t>(batch - 1));
+        knn_build_device(*tmp, kb, p.nn_descent_iterations, 0.01, mix_seed(ix.seed, n_old), g, tmp->stream);
+        std::vector<uint32_t> gid(batch * g.k);
+        std::vector<double> gsc(batch * g.k);
+        g.ids.download(gid.data(), gid.size(), tmp->stream);
+        g.scores.download(gsc.data(), gsc.size(), tmp->stream);
+        FGB_CUDA(cudaStreamSynchronize(tmp->stream));
+        for (uint64_t i = 0; i < batch; ++i)
+            for (uint32_t j = 0; j < g.k; ++j)
+                from_batch[i].push_back({static_cast<uint32_t>(n_old + gid[i * g.k + j]), gsc[i * g.k + j]});
+    }
+    for (uint64_t i = 0; i < batch; ++i)
+        if (from_index[i].size() + from_batch[i].size() < d)
+            throw Error("corpus-too-small", "doc " + std::to_string(doc_id[i]) + ": only " +
+                                                std::to_string(from_index[i].size() + from_batch[i].size()) +
+                                                " insert candidates for degree " + std::to_string(d));
+
+    // ---- append the documents (update.cpp:94-103)
+    corpus_append(c, v);
+
+    // ---- merged candidates, the per-node refinery (update.cpp:105-125)
+    std::vector<std::vector<Cand>> cands(batch);
+    for (uint64_t i = 0; i < batch; ++i) {
+        auto& cl = cands[i];
+        cl = from_index[i];
+        cl.insert(cl.end(), from_batch[i].begin(), from_batch[i].end());
+        std::sort(cl.begin(), cl.end(), [](const Cand& a, const Cand& b) {
+            if (a.score != b.score) return a.score > b.score;
+            return a.id < b.id;
+        });
+        if (cl.size() > kk) cl.resize(kk);
+    }
+    std::vector<std::vector<uint32_t>> kept(batch), recycled(batch), ordered(batch);
+    for (uint64_t i0 = 0; i0 < batch;) {  // runs of equal candidate counts share a launch
+        uint64_t i1 = i0 + 1;
+        while (i1 < batch && cands[i1].size() == cands[i0].size()) ++i1;
+        const uint32_t L = static_cast<uint32_t>(cands[i0].size());
+        const uint64_t rows = i1 - i0;
+        DevKnn g;
+        g.alloc(rows, L);
+        std::vector<uint32_t> gid(rows * L);
+        std::vector<double> gsc(rows * L);
+        for (uint64_t r = 0; r < rows; ++r)
+            for (uint32_t j = 0; j < L; ++j) {
+                gid[r * L + j] = cands[i0 + r][j].id;
+                gsc[r * L + j] = cands[i0 + r][j].score;
+            }
+        g.ids.upload(gid, s);
+        g.scores.upload(gsc, s);
+        RefineOut out;
+        refine_alloc(g, d, out, s);
+        refine_nodes(c, g, false, n_old + i0, n_old + i1, out, s, n_old + i0);
+        std::vector<uint32_t> ko(rows * d), kc(rows), ro(rows * L), rcn(rows), oo(rows * L);
+        out.kept.download(ko.data(), ko.size(), s);
+        out.kept_count.download(kc.data(), rows, s);
+        out.keyword.download(ro.data(), ro.size(), s);
+        out.kw_count.download(rcn.data(), rows, s);
+        out.ordered.download(oo.data(), oo.size(), s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t r = 0; r < rows; ++r) {
+            kept[i0 + r].assign(ko.begin() + r * d, ko.begin() + r * d + kc[r]);
+            recycled[i0 + r].assign(ro.begin() + r * L, ro.begin() + r * L + rcn[r]);
+            ordered[i0 + r].assign(oo.begin() + r * L, oo.begin() + r * L + L);
+        }
+        i0 = i1;
+    }
+
+    // ---- reverse half among the batch, new semantic / keyword lists (update.cpp:127-165)
+    const uint32_t half = d / 2;
+    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> keepers(batch);  // (pos, keeper)
+    for (uint64_t w = 0; w < batch; ++w)
+        for (size_t q = 0; q < kept[w].size(); ++q)
+            if (kept[w][q] >= n_old)
+                keepers[kept[w][q] - n_old].emplace_back(static_cast<uint32_t>(q), static_cast<uint32_t>(n_old + w));
+    const uint64_t n = n_old + batch;
+    ix.semantic_h.resize(n * d);
+    std::vector<std::vector<uint32_t>> new_kw(batch);
+    for (uint64_t i = 0; i < batch; ++i) {
+        std::vector<uint32_t> list;
+        list.reserve(d);
+        auto has = [&](uint32_t id) { return std::find(list.begin(), list.end(), id) != list.end(); };
+        const size_t forward = std::min<size_t>(half, kept[i].size());
+        for (size_t q = 0; q < forward; ++q) list.push_back(kept[i][q]);
+        std::sort(keepers[i].begin(), keepers[i].end());
+        for (const auto& [pos, w] : keepers[i]) {
+            if (list.size() >= forward + half) break;
+            if (!has(w)) list.push_back(w);
+        }
+        for (size_t q = forward; q < kept[i].size() && list.size() < d; ++q)
+            if (!has(kept[i][q])) list.push_back(kept[i][q]);
+        for (uint32_t id : ordered[i]) {
+            if (list.size() >= d) break;
+            if (!has(id)) list.push_back(id);
+        }
+        if (list.size() != d) throw Error("invariant-violation", "insert produced a short semantic list");
+        std::copy(list.begin(), list.end(), ix.semantic_h.begin() + (n_old + i) * d);
+        for (uint32_t id : recycled[i])
+            if (!has(id)) new_kw[i].push_back(id);
+    }
+
+    // ---- existing nodes: weakest reverse slot replacement (update.cpp:167-193),
+    // in the reference's order over exact pair scores computed on the GPU
+    std::vector<uint32_t> pa, pb;
+    std::vector<char> touched(n_old, 0);
+    for (uint64_t i = 0; i < batch; ++i)
+        for (uint32_t w : kept[i]) {
+            if (w >= n_old) continue;
+            if (!touched[w]) {
+                touched[w] = 1;
+                for (uint32_t sl = half; sl < d; ++sl) {
+                    pa.push_back(w);
+                    pb.push_back(ix.semantic_h[static_cast<uint64_t>(w) * d + sl]);
+                }
+            }
+            pa.push_back(w);
+            pb.push_back(static_cast<uint32_t>(n_old + i));
+        }
+    std::vector<double> ps(pa.size());
+    if (!pa.empty() &&
+        fg_pair_scores(&c, pa.data(), pb.data(), pa.size(), ps.data()) != FG_OK)
+        throw Error(fg_last_error_code(), fg_last_error_message());
+    std::unordered_map<uint64_t, double> pair_score;
+    for (size_t q = 0; q < pa.size(); ++q) pair_score[(static_cast<uint64_t>(pa[q]) << 32) | pb[q]] = ps[q];
+    std::unordered_map<uint32_t, std::vector<double>> slot_scores;
+    for (uint64_t i = 0; i < batch; ++i) {
+        const uint32_t u = static_cast<uint32_t>(n_old + i);
+        for (uint32_t w : kept[i]) {
+            if (w >= n_old) continue;
+            uint32_t* sem = ix.semantic_h.data() + static_cast<uint64_t>(w) * d;
+            if (std::find(sem, sem + d, u) != sem + d) continue;
+            auto& sc = slot_scores[w];
+            if (sc.empty()) {
+                sc.resize(d - half);
+                for (uint32_t sl = half; sl < d; ++sl)
+                    sc[sl - half] = pair_score.at((static_cast<uint64_t>(w) << 32) | sem[sl]);
+            }
+            const size_t weakest = static_cast<size_t>(std::min_element(sc.begin(), sc.end()) - sc.begin());
+            const double incoming = pair_score.at((static_cast<uint64_t>(w) << 32) | u);
+            if (incoming > sc[weakest]) {
+                sem[half + weakest] = u;
+                sc[weakest] = incoming;
+            }
+        }
+    }
+
+    // ---- keyword and logical edges, entity map, norm order; device refresh
+    HostList kw;
+    kw.ptr.assign(1, 0);
+    for (uint64_t u = 0; u < n_old; ++u) {
+        kw.idx.insert(kw.idx.end(), ix.keyword_h.begin(u), ix.keyword_h.end(u));
+        kw.ptr.push_back(kw.idx.size());
+    }
+    for (uint64_t i = 0; i < batch; ++i) {
+        kw.idx.insert(kw.idx.end(), new_kw[i].begin(), new_kw[i].end());
+        kw.ptr.push_back(kw.idx.size());
+    }
+    ix.keyword_h = std::move(kw);
+    std::vector<uint32_t> ks, kr, kt;
+    for (size_t t = 0; t + 2 < ix.triplets.size(); t += 3) {
+        ks.push_back(ix.triplets[t]);
+        kr.push_back(ix.triplets[t + 1]);
+        kt.push_back(ix.triplets[t + 2]);
+    }
+    const fg_kg_view kgv{ks.size(), ks.data(), kr.data(), kt.data()};
+    ix.entity_map.clear();  // build_entity_map order == appending the new nodes
+    for (uint64_t u = 0; u < n; ++u)
+        for (const uint32_t* e = c.entities.begin(u); e != c.entities.end(u); ++e)
+            ix.entity_map[*e].push_back(static_cast<uint32_t>(u));
+    {
+        const HostKg hk = make_kg(&kgv);
+        for (uint64_t i = 0; i < batch; ++i) {
+            std::vector<uint32_t> e;
+            logical_for(c, static_cast<uint32_t>(n_old + i), hk, ix.entity_map, ix.logical_cap, e);
+            ix.lg_h.insert(ix.lg_h.end(), e.begin(), e.end());
+            ix.lg_ptr_h.push_back(ix.lg_ptr_h.back() + e.size() / 4);
+        }
+    }
+    ix.semantic.upload(ix.semantic_h, s);
+    ix.norm_order_h.clear();  // rebuild_norm_order (index.cpp:12-23)
+    index_finish(ix, &kgv);
+}
+
+}  // namespace
 }  // namespace fgb
 
 using namespace fgb;
 
 extern "C" {
+
+int fg_index_insert(fg_index* ix, const fg_corpus_view* docs, const fg_insert_params* params) {
+    return guarded([&] {
+        if (!ix || !docs) throw Error("invalid-argument", "null pointer");
+        FGB_CUDA(cudaSetDevice(ix->corpus->device));
+        const fg_insert_params p = params ? *params : fg_insert_params{0, 10, 1};
+        insert_batch_device(*ix, *docs, p);
+    });
+}
+
 
 int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p, fg_index** out) {
     return guarded([&] {

@@ -60,7 +60,7 @@ void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool pe
 // merge_reverse_edges + keyword disjointness over every node (needs all kept lists).
 void refine_alloc(const DevKnn& g, uint32_t degree, RefineOut& out, cudaStream_t s);
 void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint64_t lo, uint64_t hi,
-                  RefineOut& out, cudaStream_t s);
+                  RefineOut& out, cudaStream_t s, uint64_t row0 = 0);
 void refine_merge(uint64_t n, RefineOut& out, cudaStream_t s);
 
 }  // namespace fgb

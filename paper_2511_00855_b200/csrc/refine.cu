@@ -76,12 +76,14 @@ struct RefineArgs {
     uint32_t kwcap;        // kept-keyword hash capacity (power of two)
     uint32_t ukw_cap;      // max keyword list length
     uint64_t lo;           // first node of this launch (vertex-range sharding)
+    uint64_t row0;         // node of row 0 of the list/output arrays (inserts: n_old)
 };
 
 __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
     const uint64_t u = a.lo + blockIdx.x;
+    const uint64_t ur = u - a.row0;  // row of u in the list / output arrays
     const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     double* P = reinterpret_cast<double*>(smem);             // k*k
     double* csc = P + k * k;                                 // k
@@ -96,8 +98,8 @@ __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs 
     __shared__ uint32_t nkept, nrec;
 
     for (uint32_t j = tid; j < k; j += nt) {
-        cid[j] = a.L_ids[u * k + j];
-        csc[j] = a.L_sc[u * k + j];
+        cid[j] = a.L_ids[ur * k + j];
+        csc[j] = a.L_sc[ur * k + j];
         P[j * k + j] = 0.0;
     }
     for (uint32_t j = tid; j < a.kwcap; j += nt) kwset[j] = kEmpty;
@@ -178,9 +180,9 @@ __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs 
     __syncthreads();
     for (uint32_t r = tid; r < k; r += nt) {
         const uint32_t v = order[r];
-        a.ordered[u * k + r] = cid[v];
-        a.ordered_sc[u * k + r] = csc[v];
-        a.detours[u * k + r] = det[v];
+        a.ordered[ur * k + r] = cid[v];
+        a.ordered_sc[ur * k + r] = csc[v];
+        a.detours[ur * k + r] = det[v];
     }
 
     // ---- IP prune walk + keyword recycling (refine.cpp:67-118), one warp
@@ -268,11 +270,11 @@ __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs 
             }
         }
         __syncwarp();
-        for (uint32_t i = lane; i < nk; i += 32) a.kept[u * a.degree + i] = cid[order[kp[i]]];
-        for (uint32_t i = lane; i < nr; i += 32) a.recycled[u * k + i] = rec[i];
+        for (uint32_t i = lane; i < nk; i += 32) a.kept[ur * a.degree + i] = cid[order[kp[i]]];
+        for (uint32_t i = lane; i < nr; i += 32) a.recycled[ur * k + i] = rec[i];
         if (lane == 0) {
-            a.kept_count[u] = nk;
-            a.rec_count[u] = nr;
+            a.kept_count[ur] = nk;
+            a.rec_count[ur] = nr;
         }
     }
 }
@@ -384,7 +386,7 @@ void refine_alloc(const DevKnn& g, uint32_t degree, RefineOut& out, cudaStream_t
 }
 
 void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint64_t lo, uint64_t hi,
-                  RefineOut& out, cudaStream_t s) {
+                  RefineOut& out, cudaStream_t s, uint64_t row0) {
     if (hi <= lo) return;
     const uint32_t k = g.k, degree = out.degree;
     uint32_t max_kw = 0;
@@ -394,7 +396,7 @@ void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint6
     while (kwcap < 2ull * max_kw * std::min(degree, k)) kwcap <<= 1;
     RefineArgs a{c.dc, k, degree, per_neighbour ? 1 : 0, g.ids.get(), g.scores.get(),
                  out.ordered.get(), out.ordered_sc.get(), out.detours.get(), out.kept.get(),
-                 out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw, lo};
+                 out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw, lo, row0};
     const size_t sm = static_cast<size_t>(k) * k * 8 + k * 8 + static_cast<size_t>(k) * kTileStride * 4 +
                       5 * k * 4 + static_cast<size_t>(kwcap) * 4 + static_cast<size_t>(max_kw) * 4 + 16;
     if (sm > 227 * 1024)

@@ -195,6 +195,15 @@ class HybridIndex:
         return dict(degree=deg.value, semantic=sem, keyword=A.CSR(kp, ki), logical_ptr=lp,
                     logical=lg, norm_order=no)
 
+    def insert(self, docs: A.Corpus, knn_k: int = 0, nn_descent_iterations: int = 10):
+        """insert_batch (update.hpp:33): append and link `docs` in place."""
+        v = docs.view()
+        p = A.InsertParams(knn_k, nn_descent_iterations, 1)
+        check(lib().fg_index_insert(self.h, C.byref(v), C.byref(p)))
+        n, d = C.c_uint64(), C.c_uint32()
+        check(lib().fg_corpus_size(self.corpus.h, C.byref(n), C.byref(d)))
+        self.corpus.n = n.value
+
     def serialize(self, path: str) -> int:
         """serialize_index (io.hpp:63): HYBGRIX1 v1, the reference's bytes."""
         nb = C.c_uint64()
