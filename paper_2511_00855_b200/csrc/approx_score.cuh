@@ -96,7 +96,7 @@ __device__ __forceinline__ double reduce_scatter8(double (&x)[8], uint32_t lane)
 // nodes' first 128 postings (idx + val, coalesced 512 B each) are in flight
 // per round trip; postings 128.. of longer rows follow in a rolled loop.
 template <bool kBitmap>
-__device__ __noinline__ double sparse_group(const uint32_t* idx, const float* val, const PathQ P, uint32_t off4,
+__device__ __forceinline__ double sparse_group(const uint32_t* idx, const float* val, const PathQ P, uint32_t off4,
                                             uint32_t nnz, uint32_t lane, uint32_t F) {
     double mine = 0.0;
     const uint4* i4 = reinterpret_cast<const uint4*>(idx);

@@ -114,6 +114,7 @@ __global__ void gather_meta_kernel(const uint4* meta, const uint32_t* ids, uint6
 
 void index_finish(fg_index& ix, const fg_kg_view* kgv) {
     fg_corpus& c = *ix.corpus;
+    ix.device = c.device;
     cudaStream_t s = c.stream;
     const uint64_t n = c.n;
     auto t0 = Clock::now();
@@ -649,7 +650,9 @@ int fg_index_build_times(const fg_index* ix, double* s5) {
 
 int fg_index_free(fg_index* ix) {
     if (ix) {
-        if (ix->corpus) cudaSetDevice(ix->corpus->device);
+        // the corpus may already be gone (garbage-collected first): use the
+        // index's own device record only
+        cudaSetDevice(ix->device);
         if (ix->ev0) cudaEventDestroy(ix->ev0);
         if (ix->ev1) cudaEventDestroy(ix->ev1);
         delete ix;

@@ -8,6 +8,7 @@
 
 struct fg_index {
     fg_corpus* corpus = nullptr;  // not owned
+    int device = 0;               // the corpus's device (freeing must not touch the corpus)
     uint32_t degree = 0, knn_k = 0, logical_cap = 64, default_hops = 2;
     uint64_t seed = 0;
 
