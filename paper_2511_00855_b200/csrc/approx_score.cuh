@@ -16,10 +16,18 @@ constexpr int kSG = 8;  // sparse rows in flight per warp round trip
 // terms use a bitmap + rank structure (membership = one word test, value
 // index = the word's prefix count + a popcount: branch-free); larger ones a
 // bit filter in front of an open-addressing hash (device_common.cuh).
+// Words of a query-term bitmap over [0, vocab): the smallest power of two W
+// with 32 * W > vocab (bits >= vocab stay zero; see q_lookup_t).
+__host__ __device__ inline uint32_t bitmap_words(uint32_t vocab) {
+    uint32_t w = 1;
+    while (32ull * w <= vocab) w <<= 1;
+    return w;
+}
+
 struct PathQ {
     uint32_t on;     // path active for this query (weight != 0, query nnz > 0)
     uint32_t vocab;  // > 0: bitmap mode over [0, vocab)
-    uint32_t wm1;    // bitmap words - 1
+    uint32_t wm1;    // bitmap words - 1 (a power of two minus one, 32 * words > vocab)
     const uint32_t* bm;
     const uint16_t* pre;
     const float* qv;  // weighted values (fp32, as build_query_vector) in ascending term order
@@ -33,10 +41,12 @@ struct PathQ {
 template <bool kBitmap>
 __device__ __forceinline__ float q_lookup_t(const PathQ& P, uint32_t t, bool& found) {
     if constexpr (kBitmap) {
-        const uint32_t tw = min(t >> 5, P.wm1);
+        // the bitmap spans a power of two of words past the vocabulary, so
+        // masking maps the padding id (0xFFFFFFFF) to a bit that is never set
+        const uint32_t tw = (t >> 5) & P.wm1;
         const uint32_t word = P.bm[tw];
         const uint32_t pre = P.pre[tw];
-        found = t < P.vocab && ((word >> (t & 31)) & 1u);
+        found = (word >> (t & 31)) & 1u;
         const float q = P.qv[pre + __popc(word & ((1u << (t & 31)) - 1u))];
         return found ? q : 0.0f;
     } else {

@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         }
         // learned path of u as a bitmap + rank structure (branch-free lookups)
         if (a.l_vocab && P[0].on) {
-            const uint32_t W = (a.l_vocab + 31) / 32;
+            const uint32_t W = approx::bitmap_words(a.l_vocab);
             uint32_t* bm = reinterpret_cast<uint32_t*>(qd + a.c.dstride);
             uint16_t* pre = reinterpret_cast<uint16_t*>(bm + ((W + 3) & ~3u));
             float* qv = reinterpret_cast<float*>(pre + ((W + 7) & ~7u));
@@ -448,7 +448,7 @@ size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uin
     b += 2 * k + 3 * k + 2 * kPassThreads + 16;          // new / exact / mark flags, alignment
     b += static_cast<size_t>(dstride) * 4;                // fp32 dense row of u
     if (l_vocab) {                                        // u's learned bitmap, prefix, values
-        const size_t W = (l_vocab + 31) / 32;
+        const size_t W = approx::bitmap_words(l_vocab);
         b += ((W + 3) & ~size_t(3)) * 4 + ((W + 7) & ~size_t(7)) * 2 + static_cast<size_t>(lcap) * 4;
     }
     return b;

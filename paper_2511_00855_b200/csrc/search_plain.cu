@@ -207,7 +207,7 @@ __host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~s
 // Bytes of one staged sparse path (PlainLaunch::vocab/cap).
 __host__ __device__ __forceinline__ size_t path_bytes(uint32_t vocab, uint32_t cap) {
     if (vocab) {
-        const size_t W = (vocab + 31) / 32;
+        const size_t W = approx::bitmap_words(vocab);
         return al16(W * 4) + al16(W * 2) + al16(cap * 4);
     }
     return al16(cap * 4) + al16(cap * 4) + al16(filter_words(cap) * 4);
@@ -246,7 +246,7 @@ __device__ double stage_path(const PlainLaunch& a, uint64_t qi, int path, unsign
     P.vocab = vocab;
     double ss = 0.0;
     if (vocab) {
-        const uint32_t W = (vocab + 31) / 32;
+        const uint32_t W = approx::bitmap_words(vocab);
         P.wm1 = W - 1;
         uint32_t* bm = reinterpret_cast<uint32_t*>(mem);
         uint16_t* pre = reinterpret_cast<uint16_t*>(mem + al16(W * 4));
