@@ -84,7 +84,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "250"],
                                       stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -197,6 +197,7 @@ def main():
     # ---- this rank's shard
     lo, hi = shard_range(queries.count, world, rank)
     shard = queries.subset(np.arange(lo, hi)).with_(beam_width=max(beam, 10))
+    shard = shard.pinned()  # e2e inputs come from page-locked host memory
     for _ in range(args.warmup):
         fg.batch_query(ix, shard, entry_count=entry)
 

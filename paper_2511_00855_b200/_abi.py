@@ -312,6 +312,35 @@ class Queries:
         v.max_entity_hops = ptr(self.max_entity_hops, u32p)
         return v
 
+    def pinned(self) -> "Queries":
+        """A copy whose arrays live in page-locked host memory (torch pinned
+        tensors), so the library's host->device copies run at full DMA speed."""
+        import torch
+
+        owners = []
+
+        def pin(a):
+            if a is None:
+                return None
+            t = torch.empty(a.shape, dtype=getattr(torch, a.dtype.name), pin_memory=True)
+            owners.append(t)  # the numpy view does not keep the tensor alive
+            out = t.numpy()
+            out[...] = a
+            return out
+
+        def pin_csr(c):
+            return None if c is None else CSR(pin(c.ptr), pin(c.idx), pin(c.val))
+
+        q = Queries.__new__(Queries)
+        q.__dict__.update(self.__dict__)
+        q.dense = pin(self.dense)
+        q.learned, q.statistical = pin_csr(self.learned), pin_csr(self.statistical)
+        q.required, q.entities = pin_csr(self.required), pin_csr(self.entities)
+        q.weights, q.k = pin(self.weights), pin(self.k)
+        q.beam_width, q.max_entity_hops = pin(self.beam_width), pin(self.max_entity_hops)
+        q._pinned = owners
+        return q
+
     def h2d_bytes(self) -> int:
         """Bytes of the query payload a search call ships to the device."""
         total = self.dense.nbytes + self.weights.nbytes + 3 * 4 * self.count

@@ -92,6 +92,31 @@ private:
     size_t n_ = 0;
 };
 
+// Grow-only page-locked host buffer (device->host staging at DMA speed).
+template <typename T>
+class PinnedBuf {
+public:
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() {
+        if (p_) cudaFreeHost(p_);
+    }
+    void ensure(size_t n) {
+        if (n <= n_) return;
+        if (p_) cudaFreeHost(p_);
+        p_ = nullptr;
+        n_ = 0;
+        FGB_CUDA(cudaMallocHost(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    T* get() const { return p_; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
 // Host-side CSR copy of a sorted-id list per row.
 struct HostList {
     std::vector<uint64_t> ptr{0};
@@ -163,6 +188,22 @@ struct QueryUpload {
     DevQueries dq{};
 
     void upload(const fg_query_view& q, cudaStream_t s);
+};
+
+// Per-index search I/O: device copies of a batch, its seeds and results, and
+// the pinned staging the results come back through. Grow-only and reused, so a
+// steady stream of batch_query calls does no cudaMalloc/cudaFree (each of those
+// synchronises the device and contends with driver clients such as nvidia-smi).
+struct SearchIo {
+    QueryUpload up;
+    DevBuf<uint64_t> sptr;
+    DevBuf<uint32_t> snode, sent;
+    DevBuf<uint8_t> shas, qflags;
+    DevBuf<uint32_t> r_node, r_count, r_warn, r_err;
+    DevBuf<double> r_score;
+    DevBuf<unsigned long long> r_exp, r_sc;
+    DevBuf<unsigned int> work;
+    PinnedBuf<unsigned char> host;
 };
 
 inline uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }

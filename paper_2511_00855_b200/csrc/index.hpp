@@ -2,6 +2,7 @@
 #pragma once
 
 #include <map>
+#include <mutex>
 #include <vector>
 
 #include "fg_cuda.hpp"
@@ -44,6 +45,8 @@ struct fg_index {
     fgb::DevBuf<uint32_t> scratch_lists;
     fgb::DevBuf<unsigned char> scratch_misc;
     uint64_t scratch_slots = 0;
+    fgb::SearchIo io;        // batch_query buffers (one call at a time: search_mu)
+    std::mutex search_mu;
     double last_kernel_ms = 0.0;
     uint64_t last_launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -1009,22 +1009,27 @@ constexpr uint64_t kId30 = 0x3FFFFFFFull;  // node ids must fit 30 bits in the p
 // Device results -> the caller's fg_search_results (ids -> doc ids, per-query
 // validation errors, counters); records the kernel time of ev0..ev1.
 void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg_search_results* out,
-                    const std::vector<std::string>& errs, uint64_t nq, uint32_t stride,
-                    const DevBuf<uint32_t>& r_node, const DevBuf<double>& r_score,
-                    const DevBuf<uint32_t>& r_count, const DevBuf<uint32_t>& r_warn,
-                    const DevBuf<uint32_t>& r_err, const DevBuf<unsigned long long>& r_exp,
-                    const DevBuf<unsigned long long>& r_sc, cudaStream_t s) {
+                    const std::vector<std::string>& errs, uint64_t nq, uint32_t stride, cudaStream_t s) {
     (void)q;
-    std::vector<uint32_t> h_node(nq * stride), h_count(nq), h_warn(nq), h_err(nq);
-    std::vector<double> h_score(nq * stride);
-    std::vector<unsigned long long> h_exp(nq), h_sc(nq);
-    r_node.download(h_node.data(), nq * stride, s);
-    r_score.download(h_score.data(), nq * stride, s);
-    r_count.download(h_count.data(), nq, s);
-    r_warn.download(h_warn.data(), nq, s);
-    r_err.download(h_err.data(), nq, s);
-    r_exp.download(h_exp.data(), nq, s);
-    r_sc.download(h_sc.data(), nq, s);
+    SearchIo& io = ix->io;
+    // pinned staging: 8-byte fields first, then the 4-byte ones
+    const uint64_t hits = nq * stride;
+    io.host.ensure(hits * 12 + nq * 32 + 16);
+    unsigned char* h = io.host.get();
+    double* h_score = reinterpret_cast<double*>(h);
+    unsigned long long* h_exp = reinterpret_cast<unsigned long long*>(h_score + hits);
+    unsigned long long* h_sc = h_exp + nq;
+    uint32_t* h_node = reinterpret_cast<uint32_t*>(h_sc + nq);
+    uint32_t* h_count = h_node + hits;
+    uint32_t* h_warn = h_count + nq;
+    uint32_t* h_err = h_warn + nq;
+    io.r_node.download(h_node, hits, s);
+    io.r_score.download(h_score, hits, s);
+    io.r_count.download(h_count, nq, s);
+    io.r_warn.download(h_warn, nq, s);
+    io.r_err.download(h_err, nq, s);
+    io.r_exp.download(h_exp, nq, s);
+    io.r_sc.download(h_sc, nq, s);
     FGB_CUDA(cudaStreamSynchronize(s));
     float ms = 0;
     FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
@@ -1062,6 +1067,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
     return guarded([&] {
         if (!cix || !q || !out) throw Error("invalid-argument", "null pointer");
         fg_index* ix = const_cast<fg_index*>(cix);
+        std::lock_guard<std::mutex> lock(ix->search_mu);
         fg_corpus& c = *ix->corpus;
         FGB_CUDA(cudaSetDevice(c.device));
         cudaStream_t s = c.stream;
@@ -1148,12 +1154,13 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             }
         }
 
-        // ---- device copies of the batch
-        QueryUpload up;
+        // ---- device copies of the batch (buffers reused across calls)
+        SearchIo& io = ix->io;
+        QueryUpload& up = io.up;
         up.upload(*q, s);
-        DevBuf<uint64_t> d_sptr;
-        DevBuf<uint32_t> d_snode, d_sent;
-        DevBuf<uint8_t> d_shas, d_qflags;
+        DevBuf<uint64_t>& d_sptr = io.sptr;
+        DevBuf<uint32_t>&d_snode = io.snode, &d_sent = io.sent;
+        DevBuf<uint8_t>&d_shas = io.shas, &d_qflags = io.qflags;
         d_sptr.upload(seed_ptr, s);
         if (seed_node.empty()) {
             seed_node.push_back(0);
@@ -1165,12 +1172,20 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         d_shas.upload(seed_has, s);
         d_qflags.upload(qflags.empty() ? std::vector<uint8_t>(1, 0) : qflags, s);
         const uint32_t stride = std::max(out->hit_stride, 1u);
-        DevBuf<uint32_t> r_node(std::max<uint64_t>(nq * stride, 1)), r_count(std::max<uint64_t>(nq, 1)),
-            r_warn(std::max<uint64_t>(nq, 1)), r_err(std::max<uint64_t>(nq, 1));
-        DevBuf<double> r_score(std::max<uint64_t>(nq * stride, 1));
-        DevBuf<unsigned long long> r_exp(std::max<uint64_t>(nq, 1)), r_sc(std::max<uint64_t>(nq, 1));
-        DevBuf<unsigned int> work(1);
-        work.zero(s);
+        const uint64_t nq1 = std::max<uint64_t>(nq, 1);
+        io.r_node.ensure(nq1 * stride);
+        io.r_score.ensure(nq1 * stride);
+        io.r_count.ensure(nq1);
+        io.r_warn.ensure(nq1);
+        io.r_err.ensure(nq1);
+        io.r_exp.ensure(nq1);
+        io.r_sc.ensure(nq1);
+        DevBuf<uint32_t>&r_node = io.r_node, &r_count = io.r_count, &r_warn = io.r_warn, &r_err = io.r_err;
+        DevBuf<double>& r_score = io.r_score;
+        DevBuf<unsigned long long>&r_exp = io.r_exp, &r_sc = io.r_sc;
+        io.work.ensure(1);
+        FGB_CUDA(cudaMemsetAsync(io.work.get(), 0, sizeof(unsigned int), s));
+        DevBuf<unsigned int>& work = io.work;
 
         // ---- plain batches (no entity context, no required keywords): the
         // certified-approximate kernel (search_plain.cu), bit-identical results
@@ -1270,8 +1285,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                         std::fprintf(stderr, "[plain stats] exact resolutions %llu, exact final entries %llu\n",
                                      st[0], st[1]);
                 }
-                finish_results(ix, c, q, out, errs, nq, stride, r_node, r_score, r_count, r_warn, r_err, r_exp,
-                               r_sc, s);
+                finish_results(ix, c, q, out, errs, nq, stride, s);
                 ix->last_launches = 1;
                 return;
             }
@@ -1393,7 +1407,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         FGB_LAUNCH("search_kernel");
         FGB_CUDA(cudaEventRecord(ix->ev1, s));
 
-        finish_results(ix, c, q, out, errs, nq, stride, r_node, r_score, r_count, r_warn, r_err, r_exp, r_sc, s);
+        finish_results(ix, c, q, out, errs, nq, stride, s);
         ix->last_launches = nq ? 1 : 0;
         if (a.timing) {
             unsigned long long t[kPhCount];

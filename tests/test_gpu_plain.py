@@ -120,3 +120,20 @@ def test_plain_deleted_and_d128(ref):
     rix = ref.index_create(ref.store(cd, kg), g, 32)
     q = synth.synth_queries(p, 64, beam_width=100)
     same(fg.batch_query(gix, q, entry_count=100), ref.batch_query(rix, q, entry_count=100))
+
+
+def test_plain_buffer_reuse_and_pinned_inputs(c2_small, ref):
+    """batch_query reuses its device/pinned buffers across calls: a large
+    batch, then a small one, then an invalid-query batch, then pinned inputs —
+    each must match the reference exactly (no stale rows from a prior call)."""
+    p, c, dc, gix, rix = c2_small
+    big = synth.synth_queries(p, 64, beam_width=64)
+    small = big.subset(np.arange(5)).with_(beam_width=32)
+    bad = small.with_(k=np.array([10, 0, 10, 10, 10], np.uint32))  # query 1: invalid-k
+    thr = os.cpu_count() or 1
+    same(fg.batch_query(gix, big, entry_count=32), ref.batch_query(rix, big, entry_count=32, threads=thr))
+    same(fg.batch_query(gix, small, entry_count=32), ref.batch_query(rix, small, entry_count=32, threads=thr))
+    g = fg.batch_query(gix, bad, entry_count=32)
+    same(g, ref.batch_query(rix, bad, entry_count=32, threads=thr))
+    assert g.error(1).startswith("invalid-k") and g.hit_count[1] == 0
+    same(fg.batch_query(gix, big.pinned(), entry_count=32), ref.batch_query(rix, big, entry_count=32, threads=thr))
