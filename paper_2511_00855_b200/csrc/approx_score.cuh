@@ -12,6 +12,10 @@ namespace approx {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kSG = 8;  // sparse rows in flight per warp round trip
 
+// One padding posting group (never matches a query term, value 0).
+static __device__ const uint4 g_pad_idx4 = {kPad, kPad, kPad, kPad};
+static __device__ const float4 g_pad_val4 = {0.f, 0.f, 0.f, 0.f};
+
 // One sparse query path staged in shared memory.  Vocabularies up to 64K
 // terms use a bitmap + rank structure (membership = one word test, value
 // index = the word's prefix count + a popcount: branch-free); larger ones a
@@ -115,22 +119,31 @@ __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float*
     for (uint32_t g = 0; g < F; g += kSG) {
         uint4 ii[kSG];
         float4 vv[kSG];
+        // unpredicated loads (lanes past a row read the shared padding
+        // record): a predicated load-or-default lets the compiler convert
+        // each value right under its load, which serialises the round trips
 #pragma unroll
         for (int k = 0; k < kSG; ++k) {
             const uint32_t j = g + k;
             const uint32_t oj = __shfl_sync(kFull, off4, j & 31);
             const uint32_t nj = __shfl_sync(kFull, nnz, j & 31);
-            if (j < F && 4 * lane < nj) {
-                ii[k] = __ldg(i4 + oj + lane);
-                vv[k] = __ldg(v4 + oj + lane);
-            } else {
-                ii[k] = make_uint4(kPad, kPad, kPad, kPad);
-                vv[k] = make_float4(0, 0, 0, 0);
-            }
+            const bool in = j < F && 4 * lane < nj;
+            ii[k] = __ldg(in ? i4 + oj + lane : &g_pad_idx4);
+            vv[k] = __ldg(in ? v4 + oj + lane : &g_pad_val4);
         }
+        // every probe depends on every load of the group (through a shuffle
+        // ptxas cannot fold), so all kSG x 2 loads are issued before the
+        // first probe instead of one pair per probe
+        uint32_t tok = 0;
+#pragma unroll
+        for (int k = 0; k < kSG; ++k) tok += ii[k].x + __float_as_uint(vv[k].x);
+        tok = __shfl_sync(kFull, tok, lane);
+        PathQ Pg = P;
+        Pg.wm1 = min(P.wm1, P.wm1 | tok);
+        Pg.mask = min(P.mask, P.mask | tok);
         double part[8];
 #pragma unroll
-        for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap>(ii[k], vv[k], P);
+        for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap>(ii[k], vv[k], Pg);
         const double r = reduce_scatter8(part, lane);
         const uint32_t k = lane - g;  // owner lane g + k takes node k's sum from lane 4k
         const double got = __shfl_sync(kFull, r, (4 * k) & 31);
@@ -157,11 +170,9 @@ template <int NQ4>
 __device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, uint32_t lane, float4 (&b)[NQ4]) {
     const float4* row = reinterpret_cast<const float4*>(c.dense + static_cast<uint64_t>(node) * c.dstride);
     const uint32_t n4 = c.dstride >> 2;
+    // (clamped, unpredicated: columns past the row are multiplied by nothing)
 #pragma unroll
-    for (int k = 0; k < NQ4; ++k) {
-        const uint32_t col = k * 32 + lane;
-        b[k] = col < n4 ? __ldg(row + col) : make_float4(0, 0, 0, 0);
-    }
+    for (int k = 0; k < NQ4; ++k) b[k] = __ldg(row + min(k * 32 + lane, n4 - 1));
 }
 
 // Warp-cooperative approximate dense dot (coalesced 512-B loads per warp

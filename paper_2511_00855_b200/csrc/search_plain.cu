@@ -53,6 +53,12 @@ using approx::sparse_group;
 constexpr int kMinWarps = 12;  // launch bound: query-warps per SM (register budget)
 enum : uint32_t { QF_VALID = 1, QF_ENTITY = 2, QF_FALLBACK = 4 };
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000ll); }
 
 __device__ __forceinline__ bool eless(double d1, uint32_t n1, double d2, uint32_t n2) {
@@ -328,6 +334,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
         }
     };
     unsigned long long resolved = 0, final_exact = 0;
+    if (kTime && lane == 0) atomicMin(&a.timing[kPlainPhStart], globaltimer());
 
 #pragma unroll 1
     while (true) {
@@ -454,8 +461,19 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             if (mine && ntouched + lane < a.tcap) touched[ntouched + lane] = cn;
             ntouched += F;
             scored += F;
-            if (mine && Q.qd && a.prefetch >= 2)
+            if (mine && Q.qd && (a.prefetch & 2))
                 l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
+            if (mine && (a.prefetch & 4)) {  // postings of the groups after the first
+#pragma unroll
+                for (int path = 0; path < 2; ++path) {
+                    const uint32_t nz = path ? (mt.z >> 16) : (mt.z & 0xFFFFu);
+                    if (Q.p[path].on && nz && lane >= kSG) {
+                        const uint64_t o = 4ull * (path ? mt.y : mt.x);
+                        l2_prefetch((path ? c.s_idx : c.l_idx) + o, ((nz + 3) & ~3u) * 4);
+                        l2_prefetch((path ? c.s_val : c.l_val) + o, ((nz + 3) & ~3u) * 4);
+                    }
+                }
+            }
             double L = 0.0, S = 0.0;
 #pragma unroll 1
             for (int path = 0; path < 2; ++path) {
@@ -483,7 +501,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                 keep = !(ub < floor);
             }
             const uint32_t km = __ballot_sync(kFull, keep);
-            if (keep && Q.qd && a.prefetch == 1)
+            if (keep && Q.qd && (a.prefetch & 1))
                 l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
             const double D = Q.qd ? dense_group<NQ4>(c, Q.qd, cn, lane, km) : 0.0;
             phase_end(kPlainPhDense);
@@ -612,6 +630,11 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             atomicAdd(&a.timing[kPlainPhQueries], 1ull);
             atomicAdd(&a.timing[kPlainPhExpanded], expanded);
         }
+    }
+    if (kTime && lane == 0) {  // the tail: spread of the query-warps' finish times
+        const unsigned long long t = globaltimer();
+        atomicMin(&a.timing[kPlainPhEndMin], t);
+        atomicMax(&a.timing[kPlainPhEndMax], t);
     }
     if (a.stats) {
         const unsigned long long fe = __reduce_add_sync(kFull, static_cast<unsigned>(final_exact));

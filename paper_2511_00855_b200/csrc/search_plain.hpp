@@ -44,7 +44,8 @@ struct PlainLaunch {
 
 enum : int {
     kPlainPhSeeds = 0, kPlainPhSelect, kPlainPhAdj, kPlainPhSparse, kPlainPhDense,
-    kPlainPhMerge, kPlainPhFinal, kPlainPhQueries, kPlainPhExpanded, kPlainPhCount
+    kPlainPhMerge, kPlainPhFinal, kPlainPhQueries, kPlainPhExpanded, kPlainPhStart, kPlainPhEndMin,
+    kPlainPhEndMax, kPlainPhCount
 };
 
 // Per-warp shared memory of the plain kernel; 0 when the batch does not fit.
