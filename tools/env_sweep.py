@@ -24,8 +24,19 @@ p = A.synth_params(docs=a.docs, dense_dim=768, learned_vocab=30522, learned_nnz=
                    statistical_vocab=0, statistical_nnz=40, seed=1)
 c, kg, _ = synth.generate_corpus(p, 0)
 dc = fg.DeviceCorpus(c)
-ix = fg.build_hybrid_index(dc, kg, degree=32, knn_k=64, knn_iterations=10, seed=42)
-print("build", ix.build_times(), flush=True)
+cache = f"/tmp/fgb_sweep_graph_{a.docs}.npz"  # reused by later commands of the same gpurun call
+if os.path.exists(cache):
+    z = np.load(cache)
+    g = dict(degree=int(z["degree"]), semantic=z["semantic"], keyword=A.CSR(z["kp"], z["ki"]),
+             logical_ptr=z["lp"], logical=z["lg"], norm_order=z["no"])
+    ix = fg.HybridIndex.from_graph(dc, g, kg)
+else:
+    ix = fg.build_hybrid_index(dc, kg, degree=32, knn_k=64, knn_iterations=10, seed=42)
+    print("build", ix.build_times(), flush=True)
+    g = ix.export()
+    np.savez(cache, degree=g["degree"], semantic=g["semantic"], kp=g["keyword"].ptr, ki=g["keyword"].idx,
+             lp=g["logical_ptr"], lg=g["logical"], no=g["norm_order"])
+print("library", os.environ.get("FGB_LIB_VARIANT", "default"), flush=True)
 q = synth.synth_queries(p, a.queries).with_(beam_width=a.beam)
 ref = None
 for spec in a.set or [""]:
@@ -40,8 +51,10 @@ for spec in a.set or [""]:
     if ref is None:
         ref = r
     same = np.array_equal(ref.node, r.node) and np.array_equal(ref.score.view(np.uint64), r.score.view(np.uint64))
+    import hashlib
+    h = hashlib.md5(r.node.tobytes() + r.score.tobytes() + r.expanded.tobytes()).hexdigest()[:12]
     print(f"{spec or 'default'}: {best:.0f} QPS kernel (best of {a.reps}), scored {r.scored.mean():.0f}, "
-          f"expanded {r.expanded.mean():.1f}, identical {same}", flush=True)
+          f"expanded {r.expanded.mean():.1f}, identical {same}, results {h}", flush=True)
     if a.timing:
         os.environ["FGB_SEARCH_TIMING"] = "1"
         fg.batch_query(ix, q, entry_count=a.entry)

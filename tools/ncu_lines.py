@@ -1,6 +1,7 @@
 """Aggregate ncu warp-stall samples per CUDA source line.
 
   python tools/ncu_lines.py <report.ncu-rep> <object.o> <ncu-kernel-regex> [top] [sass-function-substring]
+  (NCU_LINES_COLUMN="Instructions Executed" aggregates another source-page column)
 
 Exports the report's SASS source page, disassembles the kernel's cubin from
 the object with line info (nvdisasm --print-line-info), maps every sampled
@@ -25,9 +26,9 @@ def main():
     rows = list(csv.reader(io.StringIO(page)))
     hdr = rows[1]
     data = rows[2:]
-    ia, iw = hdr.index("Address"), hdr.index("Warp Stall Sampling (All Samples)")
+    ia, iw = hdr.index("Address"), hdr.index(os.environ.get("NCU_LINES_COLUMN", "Warp Stall Sampling (All Samples)"))
     base = int(data[0][ia], 16)
-    samples = {int(r[ia], 16) - base: int(r[iw]) for r in data if r[ia].startswith("0x")}
+    samples = {int(r[ia], 16) - base: int(float(r[iw] or 0)) for r in data if r[ia].startswith("0x")}
     with tempfile.TemporaryDirectory() as td:
         subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=td, check=True,
                        capture_output=True)
