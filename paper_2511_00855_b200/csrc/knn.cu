@@ -124,6 +124,13 @@ struct PassArgs {
     // + eps64 * |u| * max_norm (search_plain.cu's bound with unit weights)
     double eps32, eps64, max_dnorm, max_norm;
     uint32_t l_vocab;   // learned-path bitmap width (0: hash lookups)
+    // dev (FGB_KNN_TIMING=1): thread 0's cycles per phase + counters, summed
+    unsigned long long* timing;
+};
+
+enum : int {
+    kKnPhInit = 0, kKnPhPool, kKnPhScore, kKnPhMerge, kKnPhFinal,  // cycles (thread 0)
+    kKnCand, kKnDense, kKnEnter, kKnRounds, kKnResolved, kKnCount   // counters
 };
 
 __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uint32_t mask,
@@ -170,6 +177,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     uint8_t* S_mk = T_mk + k;
     __shared__ uint32_t S_cnt, n_mark;
     const uint32_t mask = a.pool_cap - 1;
+    long long t_mark = (a.timing && threadIdx.x == 0) ? clock64() : 0;
+    auto lap = [&](int ph) {
+        if (a.timing && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(&a.timing[ph], static_cast<unsigned long long>(t - t_mark));
+            t_mark = t;
+        }
+    };
+    auto count = [&](int slot, uint32_t v) {
+        if (a.timing && v) atomicAdd(&a.timing[slot], static_cast<unsigned long long>(v));
+    };
 
     for (uint32_t j = tid; j < a.pool_cap; j += nt) keys[j] = kEmpty;
     for (uint32_t j = tid; j < a.pool_cap / 32; j += nt) {
@@ -197,6 +215,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         atomicOr(&hbits[s >> 5], 1u << (s & 31));
     }
     __syncthreads();
+    lap(kKnPhInit);
 
     // Two-hop pool through forward + reverse adjacency (knn_graph.cpp:97-110).
     const uint32_t rc_u = a.R_cnt[u];
@@ -229,6 +248,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         pool_insert(keys, fbits, mask, h2, f1 || f2);
     }
     __syncthreads();
+    lap(kKnPhPool);
 
     // Score fresh, new candidates; merge survivors into the running top-k.
     const double unorm = a.c.dnorm[u];
@@ -289,11 +309,33 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     auto certain = [&](double va, uint8_t ea, double vb, uint8_t eb) {
         return (ea && eb) || fabs(va - vb) > 1.25 * ((ea ? 0.0 : eps) + (eb ? 0.0 : eps));
     };
-    for (uint32_t base = 0; base < a.pool_cap; base += nt) {
+    // compact the candidates (fresh, not already in L[u]) to the front of
+    // keys[]: the scoring rounds then cover only real candidates (late passes
+    // have ~100 in a 32K-slot table, and every round costs a memory round
+    // trip).  In place: a chunk's reads finish before its writes, and writes
+    // land below the slots read so far.  The result does not depend on the
+    // order candidates are scored in (the top-k of a set).
+    __shared__ uint32_t n_cand;
+    if (tid == 0) n_cand = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < a.pool_cap; base += nt) {  // pool_cap: a power of two >= nt
         const uint32_t s = base + tid;
-        const uint32_t id = s < a.pool_cap ? keys[s] : kEmpty;
+        const uint32_t id = keys[s];
         const bool cand = id != kEmpty && ((fbits[s >> 5] >> (s & 31)) & 1u) &&
                           !((hbits[s >> 5] >> (s & 31)) & 1u);
+        const uint32_t cm = __ballot_sync(0xFFFFFFFFu, cand);
+        uint32_t wb = 0;
+        if (lane == 0 && cm) wb = atomicAdd(&n_cand, static_cast<uint32_t>(__popc(cm)));
+        wb = __shfl_sync(0xFFFFFFFFu, wb, 0);
+        __syncthreads();
+        if (cand) keys[wb + __popc(cm & ((1u << lane) - 1u))] = id;
+    }
+    __syncthreads();
+    const uint32_t n_c = n_cand;
+    for (uint32_t base = 0; base < n_c; base += nt) {
+        const uint32_t s = base + tid;
+        const bool cand = s < n_c;
+        const uint32_t id = cand ? keys[s] : kEmpty;
         const double tau = T_sc[k - 1];
         const uint32_t tau_id = T_id[k - 1];
         if constexpr (NQ4 > 0) {
@@ -315,6 +357,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 // screening: the exact score is <= the bound (+ the approximation error)
                 bool keep = mine && !(score_upper_bound(unorm, (double)__uint_as_float(mt.w), L, S) + 2.0 * eps < tau_lo);
                 const uint32_t km = __ballot_sync(approx::kFull, keep);
+                if (lane == 0) {
+                    count(kKnCand, F);
+                    count(kKnDense, __popc(km));
+                }
                 const double D = approx::dense_group<NQ4>(a.c, qd, cn, lane, km);
                 const double v = __dadd_rn(__dadd_rn(D, L), S);
                 if (keep && !(v + eps < tau_lo)) {  // may enter: kept with its approximation
@@ -340,6 +386,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         __syncthreads();
         const uint32_t m = S_cnt;
         __syncthreads();  // everyone holds m before S_cnt can change again
+        lap(kKnPhScore);
+        if (tid == 0) {
+            count(kKnEnter, m);
+            count(kKnRounds, 1);
+        }
         if (m == 0) continue;
         if constexpr (NQ4 > 0) {
             // certify every comparison the rank-merge makes (S x T, S x S);
@@ -367,6 +418,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 uint32_t tm = 0;
                 for (uint32_t i = 0; i < k; ++i) tm += T_mk[i];
                 if (n_mark == 0 && tm == 0) break;
+                if (tid == 0) count(kKnResolved, n_mark + tm);
                 for (uint32_t i = tid; i < m; i += nt)
                     if (S_mk[i]) {
                         S_sc[i] = hybrid_score<2>(a.c, sq, S_id[i]);
@@ -419,6 +471,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         }
         if (tid == 0) S_cnt = 0;
         __syncthreads();
+        lap(kKnPhMerge);
     }
     // the list's entries that carry approximations get their exact scores
     // (the order among them was certified, so it is the exact order)
@@ -438,6 +491,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     }
     mine = __reduce_add_sync(0xFFFFFFFFu, mine);
     if ((tid & 31) == 0 && mine) atomicAdd(a.changed, (unsigned long long)mine);
+    lap(kKnPhFinal);
 }
 
 size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap,
@@ -568,7 +622,20 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0, 0};
+               0.0, 0.0, 0.0, 0.0, 0, nullptr};
+    DevBuf<unsigned long long> timing;
+    const char* te = std::getenv("FGB_KNN_TIMING");
+    if (te && te[0] == '1') {
+        timing.alloc(kKnCount);
+        timing.zero(s);
+        a.timing = timing.get();
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (a.timing) {
+        FGB_CUDA(cudaEventCreate(&e0));
+        FGB_CUDA(cudaEventCreate(&e1));
+        FGB_CUDA(cudaEventRecord(e0, s));
+    }
     // error bound of the approximate pair scores (search_plain's, unit weights)
     const double N = double(c.dstride) + c.max_lnnz + c.max_snnz + 2;
     const double M = (c.dstride >> 2) + 2.0 * ((std::max(c.max_lnnz, c.max_snnz) + 127) / 128) + 16;
@@ -595,6 +662,24 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         case 6: launch_pass<6>(a, blocks, sm, s); break;
         case 8: launch_pass<8>(a, blocks, sm, s); break;
         default: launch_pass<0>(a, blocks, sm, s); break;
+    }
+    if (a.timing) {
+        FGB_CUDA(cudaEventRecord(e1, s));
+        unsigned long long t[kKnCount];
+        timing.download(t, kKnCount, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        float ms = 0;
+        FGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        const double nb = double(blocks);
+        std::fprintf(stderr,
+                     "[knn pass] %llu nodes, %.1f ms, smem %zu B, pool_cap %u | cycles/node: init %.0f pool %.0f "
+                     "score %.0f merge %.0f final %.0f | per node: cand %.1f dense %.1f enter %.1f rounds %.1f "
+                     "resolved %.2f\n",
+                     (unsigned long long)blocks, ms, sm, a.pool_cap, t[kKnPhInit] / nb, t[kKnPhPool] / nb,
+                     t[kKnPhScore] / nb, t[kKnPhMerge] / nb, t[kKnPhFinal] / nb, t[kKnCand] / nb, t[kKnDense] / nb,
+                     t[kKnEnter] / nb, t[kKnRounds] / nb, t[kKnResolved] / nb);
     }
 }
 
