@@ -126,6 +126,7 @@ struct PassArgs {
     uint32_t l_vocab;   // learned-path bitmap width (0: hash lookups)
     // dev (FGB_KNN_TIMING=1): thread 0's cycles per phase + counters, summed
     unsigned long long* timing;
+    int prefetch;       // L2 prefetch of the postings of the sparse groups after the first
 };
 
 enum : int {
@@ -349,6 +350,17 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 const uint32_t cn = __shfl_sync(approx::kFull, id, src < 32 ? src : 0);
                 const bool mine = lane < F;
                 const uint4 mt = mine ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
+                if (a.prefetch && mine && lane >= approx::kSG) {
+#pragma unroll
+                    for (int pth = 0; pth < 2; ++pth) {
+                        const uint32_t nz = pth ? (mt.z >> 16) : (mt.z & 0xFFFFu);
+                        if (P[pth].on && nz) {
+                            const uint64_t o = 4ull * (pth ? mt.y : mt.x);
+                            l2_prefetch((pth ? a.c.s_idx : a.c.l_idx) + o, ((nz + 3) & ~3u) * 4);
+                            l2_prefetch((pth ? a.c.s_val : a.c.l_val) + o, ((nz + 3) & ~3u) * 4);
+                        }
+                    }
+                }
                 double L = 0.0, S = 0.0;
                 if (P[0].on)
                     L = P[0].vocab ? approx::sparse_group<true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F)
@@ -622,7 +634,8 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0, 0, nullptr};
+               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0};
+    if (const char* e = std::getenv("FGB_KNN_PREFETCH")) a.prefetch = std::atoi(e);
     DevBuf<unsigned long long> timing;
     const char* te = std::getenv("FGB_KNN_TIMING");
     if (te && te[0] == '1') {
