@@ -29,6 +29,11 @@ namespace fgb {
 namespace {
 
 constexpr int kPassThreads = 512;
+// Candidates scored between two merges grow 1, 2, then kSRounds batches of
+// kPassThreads (the first merges raise the screening threshold of a random
+// initial list quickly; later rounds amortise the merge's barriers).
+constexpr int kSRounds = 4;
+constexpr int kSCap = kSRounds * kPassThreads;  // entering candidates buffered per round
 
 // Rejection sampling (knn_graph.cpp:28-36) when 4k < n.
 __global__ void knn_sample_kernel(uint64_t n, uint32_t k, uint64_t seed, uint32_t* ids) {
@@ -164,19 +169,19 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     double* T_sc = reinterpret_cast<double*>(hbits + a.pool_cap / 32);
     double* T2_sc = T_sc + k;
     double* S_sc = T2_sc + k;
-    uint32_t* T_id = reinterpret_cast<uint32_t*>(S_sc + nt);
+    uint32_t* T_id = reinterpret_cast<uint32_t*>(S_sc + kSCap);
     uint32_t* T2_id = T_id + k;
     uint32_t* S_id = T2_id + k;
-    uint8_t* T_new = reinterpret_cast<uint8_t*>(S_id + nt);
+    uint8_t* T_new = reinterpret_cast<uint8_t*>(S_id + kSCap);
     uint8_t* T2_new = T_new + k;
     // exactness of the stored scores (1: the reference's exact value, 0: the
     // certified approximation +- eps) and resolution marks
     uint8_t* T_ex = T2_new + k;
     uint8_t* T2_ex = T_ex + k;
     uint8_t* S_ex = T2_ex + k;
-    uint8_t* T_mk = S_ex + nt;
+    uint8_t* T_mk = S_ex + kSCap;
     uint8_t* S_mk = T_mk + k;
-    __shared__ uint32_t S_cnt, n_mark;
+    __shared__ uint32_t S_cnt, n_mark, t_marked;
     const uint32_t mask = a.pool_cap - 1;
     long long t_mark = (a.timing && threadIdx.x == 0) ? clock64() : 0;
     auto lap = [&](int ph) {
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     // Score fresh, new candidates; merge survivors into the running top-k.
     const double unorm = a.c.dnorm[u];
     // u's dense row in fp32 (approximate path), after the flag arrays
-    float* qd = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(S_mk + nt) + 15) & ~uintptr_t(15));
+    float* qd = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(S_mk + kSCap) + 15) & ~uintptr_t(15));
     approx::PathQ P[2];
     double eps = 0.0;
     if constexpr (NQ4 > 0) {
@@ -333,9 +338,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     }
     __syncthreads();
     const uint32_t n_c = n_cand;
-    for (uint32_t base = 0; base < n_c; base += nt) {
-        const uint32_t s = base + tid;
-        const bool cand = s < n_c;
+    uint32_t round = 0;
+    for (uint32_t base = 0; base < n_c; ++round) {
+      const uint32_t end = min(n_c, base + (round == 0 ? 1u : round == 1 ? 2u : uint32_t(kSRounds)) * nt);
+      for (uint32_t b2 = base; b2 < end; b2 += nt) {
+        const uint32_t s = b2 + tid;
+        const bool cand = s < end;
         const uint32_t id = cand ? keys[s] : kEmpty;
         const double tau = T_sc[k - 1];
         const uint32_t tau_id = T_id[k - 1];
@@ -395,6 +403,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 }
             }
         }
+      }
+        base = end;
         __syncthreads();
         const uint32_t m = S_cnt;
         __syncthreads();  // everyone holds m before S_cnt can change again
@@ -410,14 +420,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
             while (true) {
                 for (uint32_t i = tid; i < m; i += nt) S_mk[i] = 0;
                 for (uint32_t i = tid; i < k; i += nt) T_mk[i] = 0;
-                if (tid == 0) n_mark = 0;
+                if (tid == 0) {
+                    n_mark = 0;
+                    t_marked = 0;
+                }
                 __syncthreads();
                 for (uint32_t i = tid; i < m; i += nt) {
                     bool mk = false;
                     for (uint32_t q = 0; q < k; ++q)
                         if (!certain(S_sc[i], S_ex[i], T_sc[q], T_ex[q])) {
                             mk = true;
-                            if (!T_ex[q]) T_mk[q] = 1;
+                            if (!T_ex[q]) {
+                                T_mk[q] = 1;
+                                t_marked = 1;
+                            }
                         }
                     for (uint32_t q = 0; q < m; ++q)
                         if (q != i && !certain(S_sc[i], S_ex[i], S_sc[q], S_ex[q])) mk = true;
@@ -427,10 +443,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                     }
                 }
                 __syncthreads();
-                uint32_t tm = 0;
-                for (uint32_t i = 0; i < k; ++i) tm += T_mk[i];
-                if (n_mark == 0 && tm == 0) break;
-                if (tid == 0) count(kKnResolved, n_mark + tm);
+                if (n_mark == 0 && t_marked == 0) break;
+                if (tid == 0) count(kKnResolved, n_mark + t_marked);
                 for (uint32_t i = tid; i < m; i += nt)
                     if (S_mk[i]) {
                         S_sc[i] = hybrid_score<2>(a.c, sq, S_id[i]);
@@ -510,8 +524,8 @@ size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uin
                  uint32_t l_vocab) {
     size_t b = (doc_stage_bytes(dstride, lcap, scap) + 15) & ~size_t(15);
     b += static_cast<size_t>(pool_cap) * 4 + 2 * (pool_cap / 32) * 4;
-    b += (2 * k + kPassThreads) * 8 + (2 * k + kPassThreads) * 4;
-    b += 2 * k + 3 * k + 2 * kPassThreads + 16;          // new / exact / mark flags, alignment
+    b += (2 * k + kSCap) * 8 + (2 * k + kSCap) * 4;
+    b += 2 * k + 3 * k + 2 * kSCap + 16;                  // new / exact / mark flags, alignment
     b += static_cast<size_t>(dstride) * 4;                // fp32 dense row of u
     if (l_vocab) {                                        // u's learned bitmap, prefix, values
         const size_t W = approx::bitmap_words(l_vocab);
