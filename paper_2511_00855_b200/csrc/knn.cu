@@ -224,34 +224,44 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     lap(kKnPhInit);
 
     // Two-hop pool through forward + reverse adjacency (knn_graph.cpp:97-110).
+    // u's first hops (forward list, then reverse list) are staged in shared
+    // memory (the candidate buffers are free until scoring); each thread then
+    // has kHopU second-hop loads in flight before its inserts (the pool is a
+    // set with OR-ed freshness, so insertion order does not matter).
     const uint32_t rc_u = a.R_cnt[u];
     const uint32_t nh1 = k + rc_u;
-    const uint64_t items = static_cast<uint64_t>(nh1) * (2 * k);
-    for (uint64_t it = tid; it < items; it += nt) {
-        const uint32_t h = static_cast<uint32_t>(it / (2 * k));
-        const uint32_t j = static_cast<uint32_t>(it % (2 * k));
-        uint32_t h1;
-        bool f1;
-        if (h < k) {
-            h1 = a.L_ids[u * k + h];
-            f1 = a.L_fr[u * k + h];
-        } else {
-            h1 = a.R_ids[u * k + (h - k)];
-            f1 = a.R_fr[u * k + (h - k)];
+    uint32_t* hop_id = S_id;
+    uint32_t* hop_rc = reinterpret_cast<uint32_t*>(S_sc);
+    uint8_t* hop_fr = S_ex;
+    for (uint32_t h = tid; h < nh1; h += nt) {
+        const uint32_t h1 = h < k ? a.L_ids[u * k + h] : a.R_ids[u * k + (h - k)];
+        hop_id[h] = h1;
+        hop_fr[h] = h < k ? a.L_fr[u * k + h] : a.R_fr[u * k + (h - k)];
+        hop_rc[h] = a.R_cnt[h1];
+    }
+    __syncthreads();
+    const uint32_t items = nh1 * (2 * k);
+    constexpr uint32_t kHopU = 4;
+    for (uint32_t it0 = tid; it0 < items; it0 += nt * kHopU) {
+        uint32_t h2[kHopU];
+        uint8_t f2[kHopU];
+        bool ok[kHopU], f1[kHopU];
+#pragma unroll
+        for (uint32_t q = 0; q < kHopU; ++q) {
+            const uint32_t it = min(it0 + q * nt, items - 1);
+            const uint32_t h = it / (2 * k), j = it % (2 * k);
+            const uint64_t h1 = hop_id[h];
+            const bool fwd = j < k;
+            const uint32_t jj = fwd ? j : j - k;
+            ok[q] = it0 + q * nt < items && (fwd || jj < hop_rc[h]);
+            f1[q] = hop_fr[h];
+            // (unconditional loads: jj < k stays inside h1's row)
+            h2[q] = fwd ? a.L_ids[h1 * k + jj] : a.R_ids[h1 * k + jj];
+            f2[q] = fwd ? a.L_fr[h1 * k + jj] : a.R_fr[h1 * k + jj];
         }
-        uint32_t h2;
-        bool f2;
-        if (j < k) {
-            h2 = a.L_ids[(uint64_t)h1 * k + j];
-            f2 = a.L_fr[(uint64_t)h1 * k + j];
-        } else {
-            const uint32_t jj = j - k;
-            if (jj >= a.R_cnt[h1]) continue;
-            h2 = a.R_ids[(uint64_t)h1 * k + jj];
-            f2 = a.R_fr[(uint64_t)h1 * k + jj];
-        }
-        if (h2 == u) continue;
-        pool_insert(keys, fbits, mask, h2, f1 || f2);
+#pragma unroll
+        for (uint32_t q = 0; q < kHopU; ++q)
+            if (ok[q] && h2[q] != u) pool_insert(keys, fbits, mask, h2[q], f1[q] || f2[q]);
     }
     __syncthreads();
     lap(kKnPhPool);
@@ -500,13 +510,66 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         lap(kKnPhMerge);
     }
     // the list's entries that carry approximations get their exact scores
-    // (the order among them was certified, so it is the exact order)
-    for (uint32_t i = tid; i < k; i += nt)
-        if (!T_ex[i]) {
-            T_sc[i] = hybrid_score<2>(a.c, sq, T_id[i]);
-            T_ex[i] = 1;
+    // (the order among them was certified, so it is the exact order).  Their
+    // dense rows are staged in shared memory by the whole CTA (coalesced; the
+    // pool table is free now; row stride dstride + 1 floats so one thread per
+    // row reads conflict-free), then one thread per entry runs the
+    // reference's chain (hybrid_score's arithmetic, element order unchanged).
+    if constexpr (NQ4 > 0) {
+        uint32_t* fix = S_id;
+        if (tid == 0) S_cnt = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < k; i += nt)
+            if (!T_ex[i]) fix[atomicAdd(&S_cnt, 1u)] = i;
+        __syncthreads();
+        const uint32_t n_fix = S_cnt;
+        const uint32_t rs = a.c.dstride + 1;
+        float* rows = reinterpret_cast<float*>(keys);
+        const uint32_t per = max(1u, static_cast<uint32_t>((static_cast<size_t>(a.pool_cap) * 4) / (rs * 4ull)));
+        const uint32_t warp = tid >> 5, nwarps = nt >> 5;
+        for (uint32_t b0 = 0; b0 < n_fix; b0 += per) {
+            const uint32_t nb = min(per, n_fix - b0);
+            for (uint32_t r = warp; r < nb; r += nwarps) {
+                // one row: NQ4 coalesced 16-B loads per lane in flight, then the stores
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.c.dense + static_cast<uint64_t>(T_id[fix[b0 + r]]) * a.c.dstride);
+                const uint32_t n4 = a.c.dstride >> 2;
+                float4 v[NQ4];
+#pragma unroll
+                for (int q = 0; q < NQ4; ++q) v[q] = __ldg(src + min(q * 32 + lane, n4 - 1));
+#pragma unroll
+                for (int q = 0; q < NQ4; ++q) {
+                    const uint32_t c4 = q * 32 + lane;
+                    if (c4 < n4) {
+                        float* d = rows + r * rs + 4 * c4;
+                        d[0] = v[q].x;
+                        d[1] = v[q].y;
+                        d[2] = v[q].z;
+                        d[3] = v[q].w;
+                    }
+                }
+            }
+            __syncthreads();
+            for (uint32_t r = tid; r < nb; r += nt) {
+                const uint32_t e = fix[b0 + r];
+                const uint32_t node = T_id[e];
+                const float* row = rows + r * rs;
+                double acc = 0.0;
+#pragma unroll 8
+                for (uint32_t j = 0; j < a.c.dstride; ++j)
+                    acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(row[j])));
+                acc = __dadd_rn(acc, sq.lmask ? sparse_chain(a.c.l_idx, a.c.l_val, a.c.l_off[node], a.c.l_nnz[node],
+                                                             sq.lkeys, sq.lvals, sq.lmask, sq.lfilt)
+                                              : 0.0);
+                acc = __dadd_rn(acc, sq.smask ? sparse_chain(a.c.s_idx, a.c.s_val, a.c.s_off[node], a.c.s_nnz[node],
+                                                             sq.skeys, sq.svals, sq.smask, sq.sfilt)
+                                              : 0.0);
+                T_sc[e] = acc;
+                T_ex[e] = 1;
+            }
+            __syncthreads();
         }
-    __syncthreads();
+    }
 
     uint32_t mine = 0;
     for (uint32_t i = tid; i < k; i += nt) {
