@@ -66,20 +66,31 @@ __device__ __forceinline__ float q_lookup(const PathQ& P, uint32_t t, bool& foun
 }
 
 // ------------------------------------------------------------ scoring
-// Exact fp64 products of the query terms among 4 postings, summed in fp64
-// (each product predicated on the lookup hit: no branches, no conversions
-// for misses).
-template <bool kBitmap>
+// The query terms among 4 postings.  kF32 = false: exact fp64 products summed
+// in fp64 (each product predicated on the lookup hit).  kF32 = true: fp32
+// products accumulated by FMA (a missing term contributes q = 0), converted
+// once — |error| <= gamma_4 (fp32) * sum|q_i v_i| <= gamma_4 |q_sparse| |d|,
+// which the caller's bound must carry (knn.cu; the search keeps fp64: its
+// tighter bound resolves 14x fewer comparisons exactly).
+template <bool kBitmap, bool kF32 = false>
 __device__ __forceinline__ double probe4(const uint4& ii, const float4& vv, const PathQ& P) {
     bool f0, f1, f2, f3;
     const float q0 = q_lookup_t<kBitmap>(P, ii.x, f0), q1 = q_lookup_t<kBitmap>(P, ii.y, f1);
     const float q2 = q_lookup_t<kBitmap>(P, ii.z, f2), q3 = q_lookup_t<kBitmap>(P, ii.w, f3);
-    double s = 0.0;
-    if (f0) s = __fma_rn((double)q0, (double)vv.x, s);
-    if (f1) s = __fma_rn((double)q1, (double)vv.y, s);
-    if (f2) s = __fma_rn((double)q2, (double)vv.z, s);
-    if (f3) s = __fma_rn((double)q3, (double)vv.w, s);
-    return s;
+    if constexpr (kF32) {
+        float s = q0 * vv.x;
+        s = __fmaf_rn(q1, vv.y, s);
+        s = __fmaf_rn(q2, vv.z, s);
+        s = __fmaf_rn(q3, vv.w, s);
+        return static_cast<double>(s);
+    } else {
+        double s = 0.0;
+        if (f0) s = __fma_rn((double)q0, (double)vv.x, s);
+        if (f1) s = __fma_rn((double)q1, (double)vv.y, s);
+        if (f2) s = __fma_rn((double)q2, (double)vv.z, s);
+        if (f3) s = __fma_rn((double)q3, (double)vv.w, s);
+        return s;
+    }
 }
 
 // Reduce-scatter of kSG per-lane partial sums: node k's total (over all 32
@@ -109,7 +120,7 @@ __device__ __forceinline__ double reduce_scatter8(double (&x)[8], uint32_t lane)
 // by lanes 0..F-1 ((off4, nnz) each); lane j receives node j's sum.  kSG
 // nodes' first 128 postings (idx + val, coalesced 512 B each) are in flight
 // per round trip; postings 128.. of longer rows follow in a rolled loop.
-template <bool kBitmap>
+template <bool kBitmap, bool kF32 = false>
 __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float* val, const PathQ P, uint32_t off4,
                                             uint32_t nnz, uint32_t lane, uint32_t F) {
     double mine = 0.0;
@@ -143,7 +154,7 @@ __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float*
         Pg.mask = min(P.mask, P.mask | tok);
         double part[8];
 #pragma unroll
-        for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap>(ii[k], vv[k], Pg);
+        for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap, kF32>(ii[k], vv[k], Pg);
         const double r = reduce_scatter8(part, lane);
         const uint32_t k = lane - g;  // owner lane g + k takes node k's sum from lane 4k
         const double got = __shfl_sync(kFull, r, (4 * k) & 31);
@@ -158,7 +169,7 @@ __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float*
         const uint32_t oj = __shfl_sync(kFull, off4, j), nj = __shfl_sync(kFull, nnz, j);
         double e = 0.0;
         for (uint32_t base = 32; 4 * base < nj; base += 32)
-            if (4 * (base + lane) < nj) e += probe4<kBitmap>(__ldg(i4 + oj + base + lane), __ldg(v4 + oj + base + lane), P);
+            if (4 * (base + lane) < nj) e += probe4<kBitmap, kF32>(__ldg(i4 + oj + base + lane), __ldg(v4 + oj + base + lane), P);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
         if (lane == j) mine += e;

@@ -221,11 +221,11 @@ __device__ __forceinline__ void probe_term(uint32_t t, float v, const uint32_t* 
 // Sparse dot: walk the document row in ascending index order and probe the
 // query's filter+hash; matches accumulate in ascending shared-index order,
 // exactly the merge/probe order of sparse_dot_impl (scoring.cpp:24-74).
+template <uint32_t kStage = 4>  // kStage x 4 entries per stage, the next stage in flight
 __device__ __forceinline__ double sparse_chain(const uint32_t* idx, const float* val, uint64_t off,
                                                uint32_t nnz, const uint32_t* keys,
                                                const float* vals, uint32_t mask,
                                                const uint32_t* filt) {
-    constexpr uint32_t kStage = 4;  // 16 entries per stage, next stage in flight
     double acc = 0.0;
     const uint4* i4 = reinterpret_cast<const uint4*>(idx + off);
     const float4* v4 = reinterpret_cast<const float4*>(val + off);

@@ -125,7 +125,7 @@ struct PassArgs {
     uint32_t pool_cap;  // power of two
     uint32_t lcap, scap;
     uint64_t lo;        // first node of this launch (vertex-range sharding)
-    // certified screening (NQ4 > 0): |approx - exact| <= eps32 * |u_d| * max_dnorm
+    // certified screening (NQ4 > 0): |approx - exact| <= eps32 * (|u_d| * max_dnorm + |u| * max_norm)
     // + eps64 * |u| * max_norm (search_plain.cu's bound with unit weights)
     double eps32, eps64, max_dnorm, max_norm;
     uint32_t l_vocab;   // learned-path bitmap width (0: hash lookups)
@@ -135,7 +135,7 @@ struct PassArgs {
 };
 
 enum : int {
-    kKnPhInit = 0, kKnPhPool, kKnPhScore, kKnPhMerge, kKnPhFinal,  // cycles (thread 0)
+    kKnPhInit = 0, kKnPhPool, kKnPhScore, kKnPhMerge, kKnPhExact, kKnPhFinal,  // cycles (thread 0)
     kKnCand, kKnDense, kKnEnter, kKnRounds, kKnResolved, kKnCount   // counters
 };
 
@@ -148,6 +148,69 @@ __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uin
         s = (s + 1) & mask;
     }
     if (fresh) atomicOr(&fbits[s >> 5], 1u << (s & 31));
+}
+
+// Exact scores (hybrid_score's arithmetic, element order unchanged) of the
+// list entries fix[0..n) (bit 31 set: T[index], else S[index]).  The dense
+// rows are staged into `rows` (room for `cap` rows of stride dstride + 1
+// floats: one thread per row then reads conflict-free) by the whole CTA with
+// coalesced 16-B loads; one thread per entry runs the chain from shared
+// memory (a chain streamed from global memory waits on ~100 dependent
+// stages).  Every thread of the CTA calls it.
+template <int NQ4>
+__device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint32_t* fix, uint32_t n,
+                              unsigned char* area, size_t area_bytes, double* T_sc, uint8_t* T_ex,
+                              const uint32_t* T_id, double* S_sc, uint8_t* S_ex, const uint32_t* S_id) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    const uint32_t rs = a.c.dstride + 1, n4 = a.c.dstride >> 2;
+    const uint32_t cap = max(1u, static_cast<uint32_t>(area_bytes / (rs * 4ull)));
+    float* rows = reinterpret_cast<float*>(area);
+    auto node_of = [&](uint32_t code) { return (code >> 31) ? T_id[code & 0x7FFFFFFFu] : S_id[code]; };
+    for (uint32_t b0 = 0; b0 < n; b0 += cap) {
+        const uint32_t nb = min(cap, n - b0);
+        for (uint32_t r = warp; r < nb; r += nwarps) {
+            const float4* src =
+                reinterpret_cast<const float4*>(a.c.dense + static_cast<uint64_t>(node_of(fix[b0 + r])) * a.c.dstride);
+            float4 v[NQ4];
+#pragma unroll
+            for (int q = 0; q < NQ4; ++q) v[q] = __ldg(src + min(q * 32 + lane, n4 - 1));
+#pragma unroll
+            for (int q = 0; q < NQ4; ++q) {
+                const uint32_t c4 = q * 32 + lane;
+                if (c4 < n4) {
+                    float* d = rows + r * rs + 4 * c4;
+                    d[0] = v[q].x;
+                    d[1] = v[q].y;
+                    d[2] = v[q].z;
+                    d[3] = v[q].w;
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t r = tid; r < nb; r += nt) {
+            const uint32_t code = fix[b0 + r];
+            const uint32_t node = node_of(code);
+            const float* row = rows + r * rs;
+            double acc = 0.0;
+#pragma unroll 8
+            for (uint32_t j = 0; j < a.c.dstride; ++j)
+                acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(row[j])));
+            acc = __dadd_rn(acc, sq.lmask ? sparse_chain(a.c.l_idx, a.c.l_val, a.c.l_off[node], a.c.l_nnz[node],
+                                                         sq.lkeys, sq.lvals, sq.lmask, sq.lfilt)
+                                          : 0.0);
+            acc = __dadd_rn(acc, sq.smask ? sparse_chain(a.c.s_idx, a.c.s_val, a.c.s_off[node], a.c.s_nnz[node],
+                                                         sq.skeys, sq.svals, sq.smask, sq.sfilt)
+                                          : 0.0);
+            if (code >> 31) {
+                T_sc[code & 0x7FFFFFFFu] = acc;
+                T_ex[code & 0x7FFFFFFFu] = 1;
+            } else {
+                S_sc[code] = acc;
+                S_ex[code] = 1;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // One NN-Descent pass for node u = lo + blockIdx.x.  NQ4 > 0: candidates
@@ -316,6 +379,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
             P[0].qv = qv;
         }
         eps = a.eps32 * unorm * (1.0 + 1e-10) * a.max_dnorm +
+              a.eps32 * sqrt(a.c.sqnorm[u]) * (1.0 + 1e-10) * a.max_norm +  // fp32 sparse products
               a.eps64 * sqrt(a.c.sqnorm[u]) * (1.0 + 1e-10) * a.max_norm + 1e-300;
         __syncthreads();
     }
@@ -381,9 +445,9 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 }
                 double L = 0.0, S = 0.0;
                 if (P[0].on)
-                    L = P[0].vocab ? approx::sparse_group<true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F)
-                                   : approx::sparse_group<false>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
-                if (P[1].on) S = approx::sparse_group<false>(a.c.s_idx, a.c.s_val, P[1], mt.y, mt.z >> 16, lane, F);
+                    L = P[0].vocab ? approx::sparse_group<true, true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F)
+                                   : approx::sparse_group<false, true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
+                if (P[1].on) S = approx::sparse_group<false, true>(a.c.s_idx, a.c.s_val, P[1], mt.y, mt.z >> 16, lane, F);
                 // screening: the exact score is <= the bound (+ the approximation error)
                 bool keep = mine && !(score_upper_bound(unorm, (double)__uint_as_float(mt.w), L, S) + 2.0 * eps < tau_lo);
                 const uint32_t km = __ballot_sync(approx::kFull, keep);
@@ -455,16 +519,26 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 __syncthreads();
                 if (n_mark == 0 && t_marked == 0) break;
                 if (tid == 0) count(kKnResolved, n_mark + t_marked);
-                for (uint32_t i = tid; i < m; i += nt)
-                    if (S_mk[i]) {
-                        S_sc[i] = hybrid_score<2>(a.c, sq, S_id[i]);
-                        S_ex[i] = 1;
+                // resolve through rows staged above the compacted candidate
+                // list (the pool's upper part and its flag words are free)
+                uint32_t* fixl = fbits;  // pool_cap / 16 words >= kSCap
+                unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_c + 3) & ~3u));
+                const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_c + 3) & ~3u)) * 4;
+                for (int lst = 0; lst < 2; ++lst) {
+                    __syncthreads();  // every thread has read the previous count
+                    if (tid == 0) n_mark = 0;
+                    __syncthreads();
+                    if (lst == 0) {
+                        for (uint32_t i = tid; i < m; i += nt)
+                            if (S_mk[i]) fixl[atomicAdd(&n_mark, 1u)] = i;
+                    } else {
+                        for (uint32_t i = tid; i < k; i += nt)
+                            if (T_mk[i]) fixl[atomicAdd(&n_mark, 1u)] = 0x80000000u | i;
                     }
-                for (uint32_t i = tid; i < k; i += nt)
-                    if (T_mk[i]) {
-                        T_sc[i] = hybrid_score<2>(a.c, sq, T_id[i]);
-                        T_ex[i] = 1;
-                    }
+                    __syncthreads();
+                    const uint32_t nf = n_mark;
+                    if (nf) exact_entries<NQ4>(a, sq, fixl, nf, area, area_bytes, T_sc, T_ex, T_id, S_sc, S_ex, S_id);
+                }
                 __syncthreads();
             }
         }
@@ -516,60 +590,18 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     // row reads conflict-free), then one thread per entry runs the
     // reference's chain (hybrid_score's arithmetic, element order unchanged).
     if constexpr (NQ4 > 0) {
-        uint32_t* fix = S_id;
+        uint32_t* fixl = fbits;
         if (tid == 0) S_cnt = 0;
         __syncthreads();
         for (uint32_t i = tid; i < k; i += nt)
-            if (!T_ex[i]) fix[atomicAdd(&S_cnt, 1u)] = i;
+            if (!T_ex[i]) fixl[atomicAdd(&S_cnt, 1u)] = 0x80000000u | i;
         __syncthreads();
         const uint32_t n_fix = S_cnt;
-        const uint32_t rs = a.c.dstride + 1;
-        float* rows = reinterpret_cast<float*>(keys);
-        const uint32_t per = max(1u, static_cast<uint32_t>((static_cast<size_t>(a.pool_cap) * 4) / (rs * 4ull)));
-        const uint32_t warp = tid >> 5, nwarps = nt >> 5;
-        for (uint32_t b0 = 0; b0 < n_fix; b0 += per) {
-            const uint32_t nb = min(per, n_fix - b0);
-            for (uint32_t r = warp; r < nb; r += nwarps) {
-                // one row: NQ4 coalesced 16-B loads per lane in flight, then the stores
-                const float4* src = reinterpret_cast<const float4*>(
-                    a.c.dense + static_cast<uint64_t>(T_id[fix[b0 + r]]) * a.c.dstride);
-                const uint32_t n4 = a.c.dstride >> 2;
-                float4 v[NQ4];
-#pragma unroll
-                for (int q = 0; q < NQ4; ++q) v[q] = __ldg(src + min(q * 32 + lane, n4 - 1));
-#pragma unroll
-                for (int q = 0; q < NQ4; ++q) {
-                    const uint32_t c4 = q * 32 + lane;
-                    if (c4 < n4) {
-                        float* d = rows + r * rs + 4 * c4;
-                        d[0] = v[q].x;
-                        d[1] = v[q].y;
-                        d[2] = v[q].z;
-                        d[3] = v[q].w;
-                    }
-                }
-            }
-            __syncthreads();
-            for (uint32_t r = tid; r < nb; r += nt) {
-                const uint32_t e = fix[b0 + r];
-                const uint32_t node = T_id[e];
-                const float* row = rows + r * rs;
-                double acc = 0.0;
-#pragma unroll 8
-                for (uint32_t j = 0; j < a.c.dstride; ++j)
-                    acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(row[j])));
-                acc = __dadd_rn(acc, sq.lmask ? sparse_chain(a.c.l_idx, a.c.l_val, a.c.l_off[node], a.c.l_nnz[node],
-                                                             sq.lkeys, sq.lvals, sq.lmask, sq.lfilt)
-                                              : 0.0);
-                acc = __dadd_rn(acc, sq.smask ? sparse_chain(a.c.s_idx, a.c.s_val, a.c.s_off[node], a.c.s_nnz[node],
-                                                             sq.skeys, sq.svals, sq.smask, sq.sfilt)
-                                              : 0.0);
-                T_sc[e] = acc;
-                T_ex[e] = 1;
-            }
-            __syncthreads();
-        }
+        if (n_fix)
+            exact_entries<NQ4>(a, sq, fixl, n_fix, reinterpret_cast<unsigned char*>(keys), size_t(a.pool_cap) * 4,
+                               T_sc, T_ex, T_id, S_sc, S_ex, S_id);
     }
+    lap(kKnPhExact);
 
     uint32_t mine = 0;
     for (uint32_t i = tid; i < k; i += nt) {
@@ -765,10 +797,10 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         const double nb = double(blocks);
         std::fprintf(stderr,
                      "[knn pass] %llu nodes, %.1f ms, smem %zu B, pool_cap %u | cycles/node: init %.0f pool %.0f "
-                     "score %.0f merge %.0f final %.0f | per node: cand %.1f dense %.1f enter %.1f rounds %.1f "
+                     "score %.0f merge %.0f exact %.0f final %.0f | per node: cand %.1f dense %.1f enter %.1f rounds %.1f "
                      "resolved %.2f\n",
                      (unsigned long long)blocks, ms, sm, a.pool_cap, t[kKnPhInit] / nb, t[kKnPhPool] / nb,
-                     t[kKnPhScore] / nb, t[kKnPhMerge] / nb, t[kKnPhFinal] / nb, t[kKnCand] / nb, t[kKnDense] / nb,
+                     t[kKnPhScore] / nb, t[kKnPhMerge] / nb, t[kKnPhExact] / nb, t[kKnPhFinal] / nb, t[kKnCand] / nb, t[kKnDense] / nb,
                      t[kKnEnter] / nb, t[kKnRounds] / nb, t[kKnResolved] / nb);
     }
 }
