@@ -163,9 +163,24 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
                               const uint32_t* T_id, double* S_sc, uint8_t* S_ex, const uint32_t* S_id) {
     const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const uint32_t rs = a.c.dstride + 1, n4 = a.c.dstride >> 2;
-    const uint32_t cap = max(1u, static_cast<uint32_t>(area_bytes / (rs * 4ull)));
+    const uint32_t cap = static_cast<uint32_t>(area_bytes / (rs * 4ull));
     float* rows = reinterpret_cast<float*>(area);
     auto node_of = [&](uint32_t code) { return (code >> 31) ? T_id[code & 0x7FFFFFFFu] : S_id[code]; };
+    if (cap == 0) {  // no room for a row (tiny pools): the chain from global memory
+        for (uint32_t r = tid; r < n; r += nt) {
+            const uint32_t code = fix[r];
+            const double acc = hybrid_score<2>(a.c, sq, node_of(code));
+            if (code >> 31) {
+                T_sc[code & 0x7FFFFFFFu] = acc;
+                T_ex[code & 0x7FFFFFFFu] = 1;
+            } else {
+                S_sc[code] = acc;
+                S_ex[code] = 1;
+            }
+        }
+        __syncthreads();
+        return;
+    }
     for (uint32_t b0 = 0; b0 < n; b0 += cap) {
         const uint32_t nb = min(cap, n - b0);
         for (uint32_t r = warp; r < nb; r += nwarps) {
@@ -211,6 +226,36 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
         }
         __syncthreads();
     }
+}
+
+// Resolves every entry whose mark is set (mk[0..cnt), tflag = bit 31 for the
+// T list) in chunks of at most capf gathered into fixl (the pool's flag
+// words: pool_cap / 16 of them, fewer than a round's entries for small pools).
+template <int NQ4>
+__device__ void resolve_marked(const PassArgs& a, const SmemQuery& sq, uint8_t* mk, uint32_t cnt, uint32_t tflag,
+                               uint32_t* fixl, uint32_t capf, uint32_t* counter, unsigned char* area,
+                               size_t area_bytes, double* T_sc, uint8_t* T_ex, const uint32_t* T_id, double* S_sc,
+                               uint8_t* S_ex, const uint32_t* S_id) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    while (true) {
+        __syncthreads();  // every thread has read the previous count
+        if (tid == 0) *counter = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < cnt; i += nt)
+            if (mk[i]) {
+                const uint32_t slot = atomicAdd(counter, 1u);
+                if (slot < capf) {
+                    fixl[slot] = tflag | i;
+                    mk[i] = 0;
+                }
+            }
+        __syncthreads();
+        const uint32_t total = *counter;
+        const uint32_t nf = min(total, capf);
+        if (nf) exact_entries<NQ4>(a, sq, fixl, nf, area, area_bytes, T_sc, T_ex, T_id, S_sc, S_ex, S_id);
+        if (total <= capf) break;
+    }
+    __syncthreads();
 }
 
 // One NN-Descent pass for node u = lo + blockIdx.x.  NQ4 > 0: candidates
@@ -521,25 +566,12 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 if (tid == 0) count(kKnResolved, n_mark + t_marked);
                 // resolve through rows staged above the compacted candidate
                 // list (the pool's upper part and its flag words are free)
-                uint32_t* fixl = fbits;  // pool_cap / 16 words >= kSCap
                 unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_c + 3) & ~3u));
                 const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_c + 3) & ~3u)) * 4;
-                for (int lst = 0; lst < 2; ++lst) {
-                    __syncthreads();  // every thread has read the previous count
-                    if (tid == 0) n_mark = 0;
-                    __syncthreads();
-                    if (lst == 0) {
-                        for (uint32_t i = tid; i < m; i += nt)
-                            if (S_mk[i]) fixl[atomicAdd(&n_mark, 1u)] = i;
-                    } else {
-                        for (uint32_t i = tid; i < k; i += nt)
-                            if (T_mk[i]) fixl[atomicAdd(&n_mark, 1u)] = 0x80000000u | i;
-                    }
-                    __syncthreads();
-                    const uint32_t nf = n_mark;
-                    if (nf) exact_entries<NQ4>(a, sq, fixl, nf, area, area_bytes, T_sc, T_ex, T_id, S_sc, S_ex, S_id);
-                }
-                __syncthreads();
+                resolve_marked<NQ4>(a, sq, S_mk, m, 0u, fbits, a.pool_cap / 16, &n_mark, area, area_bytes, T_sc,
+                                    T_ex, T_id, S_sc, S_ex, S_id);
+                resolve_marked<NQ4>(a, sq, T_mk, k, 0x80000000u, fbits, a.pool_cap / 16, &n_mark, area, area_bytes,
+                                    T_sc, T_ex, T_id, S_sc, S_ex, S_id);
             }
         }
         // rank-merge T (sorted) with S (unsorted); ids are pairwise distinct
@@ -590,16 +622,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     // row reads conflict-free), then one thread per entry runs the
     // reference's chain (hybrid_score's arithmetic, element order unchanged).
     if constexpr (NQ4 > 0) {
-        uint32_t* fixl = fbits;
-        if (tid == 0) S_cnt = 0;
-        __syncthreads();
-        for (uint32_t i = tid; i < k; i += nt)
-            if (!T_ex[i]) fixl[atomicAdd(&S_cnt, 1u)] = 0x80000000u | i;
-        __syncthreads();
-        const uint32_t n_fix = S_cnt;
-        if (n_fix)
-            exact_entries<NQ4>(a, sq, fixl, n_fix, reinterpret_cast<unsigned char*>(keys), size_t(a.pool_cap) * 4,
-                               T_sc, T_ex, T_id, S_sc, S_ex, S_id);
+        for (uint32_t i = tid; i < k; i += nt) T_mk[i] = !T_ex[i];
+        resolve_marked<NQ4>(a, sq, T_mk, k, 0x80000000u, fbits, a.pool_cap / 16, &n_mark,
+                            reinterpret_cast<unsigned char*>(keys), size_t(a.pool_cap) * 4, T_sc, T_ex, T_id, S_sc,
+                            S_ex, S_id);
     }
     lap(kKnPhExact);
 
