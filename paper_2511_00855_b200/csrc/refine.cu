@@ -30,20 +30,51 @@ constexpr uint32_t kTile = 64;        // dense floats per staged chunk
 constexpr uint32_t kTileStride = kTile + 1;
 constexpr int kMaxPairsPerThread = 8;
 
+// Sparse pair dot by merge-join (ascending term ids, matching products in
+// order).  Rows start on 4-posting boundaries and are padded with kPad, so
+// each side streams 16-B vectors with the next one already in flight: a
+// dependent global load every 4 steps instead of every step.
+__device__ __forceinline__ uint32_t lane4(const uint4& v, uint32_t i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
 __device__ double merge_dot(const uint32_t* idx, const float* val, uint64_t oa, uint32_t na,
                             uint64_t ob, uint32_t nb) {
     double acc = 0.0;
+    if (na == 0 || nb == 0) return acc;
+    const uint4* A4 = reinterpret_cast<const uint4*>(idx + oa);
+    const uint4* B4 = reinterpret_cast<const uint4*>(idx + ob);
+    const uint32_t na4 = (na + 3) >> 2, nb4 = (nb + 3) >> 2;
+    const uint4 pad = make_uint4(kPad, kPad, kPad, kPad);
+    uint4 ca = __ldg(A4), cb = __ldg(B4);
+    uint4 xa = na4 > 1 ? __ldg(A4 + 1) : pad, xb = nb4 > 1 ? __ldg(B4 + 1) : pad;
     uint32_t i = 0, j = 0;
+    auto step_a = [&] {
+        ++i;
+        if ((i & 3) == 0) {
+            ca = xa;
+            const uint32_t nx = (i >> 2) + 1;
+            xa = nx < na4 ? __ldg(A4 + nx) : pad;
+        }
+    };
+    auto step_b = [&] {
+        ++j;
+        if ((j & 3) == 0) {
+            cb = xb;
+            const uint32_t nx = (j >> 2) + 1;
+            xb = nx < nb4 ? __ldg(B4 + nx) : pad;
+        }
+    };
     while (i < na && j < nb) {
-        const uint32_t a = idx[oa + i], b = idx[ob + j];
+        const uint32_t a = lane4(ca, i & 3), b = lane4(cb, j & 3);
         if (a < b) {
-            ++i;
+            step_a();
         } else if (b < a) {
-            ++j;
+            step_b();
         } else {
             acc = __fma_rn((double)val[oa + i], (double)val[ob + j], acc);
-            ++i;
-            ++j;
+            step_a();
+            step_b();
         }
     }
     return acc;
