@@ -286,19 +286,35 @@ def main():
 
 def sweep_operating_points(fg, ix, ev, truth, args):
     """recall@10 / kernel QPS over entry_count x beam; per entry_count the beam
-    sweep stops at the first beam reaching 0.9 (larger beams only cost more)."""
+    sweep stops at the first power-of-two beam reaching 0.9 (larger beams only
+    cost more), then bisects (steps of 16) between it and the beam below."""
     rows = []
     entries = [args.entry] if args.entry else ENTRIES
     beams = [args.beam] if args.beam else BEAMS
+
+    def point(e, b):
+        r = fg.batch_query(ix, ev.with_(beam_width=max(b, 10)), entry_count=e)
+        rec = float(np.mean([fg.recall_at_k(r.ids(i), truth.ids(i), 10) for i in range(ev.count)]))
+        ms, _ = ix.last_search_stats()
+        rows.append({"entry": e, "beam": b, "recall": round(rec, 4),
+                     "qps_kernel": round(ev.count / (ms / 1e3), 1)})
+        return rec
+
     for e in entries:
+        lo = 0
         for b in beams:
-            r = fg.batch_query(ix, ev.with_(beam_width=max(b, 10)), entry_count=e)
-            rec = float(np.mean([fg.recall_at_k(r.ids(i), truth.ids(i), 10) for i in range(ev.count)]))
-            ms, _ = ix.last_search_stats()
-            rows.append({"entry": e, "beam": b, "recall": round(rec, 4),
-                         "qps_kernel": round(ev.count / (ms / 1e3), 1)})
-            if rec >= 0.9:
+            if point(e, b) >= 0.9:
+                hi = b
+                while not args.beam and hi - lo > 32:
+                    mid = (lo + hi) // 32 * 16
+                    if mid <= lo or mid >= hi:
+                        break
+                    if point(e, mid) >= 0.9:
+                        hi = mid
+                    else:
+                        lo = mid
                 break
+            lo = b
     return rows
 
 
