@@ -29,6 +29,11 @@ constexpr int kRefineThreads = 256;
 constexpr uint32_t kTile = 64;        // dense floats per staged chunk
 constexpr uint32_t kTileStride = kTile + 1;
 constexpr int kMaxPairsPerThread = 8;
+constexpr uint32_t kTileD = 32;       // dense doubles per staged chunk (even-k Gram)
+// staged-tile region (floats): the odd-k row tile or the even-k transposed double tile
+__host__ __device__ constexpr uint32_t tile_floats(uint32_t k) {
+    return k * kTileStride > kTileD * (k + 2) * 2 ? k * kTileStride : kTileD * (k + 2) * 2;
+}
 
 // Sparse pair dot by merge-join (ascending term ids, matching products in
 // order).  Rows start on 4-posting boundaries and are padded with kPad, so
@@ -110,36 +115,10 @@ struct RefineArgs {
     uint64_t row0;         // node of row 0 of the list/output arrays (inserts: n_old)
 };
 
-__global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const uint32_t k = a.k;
-    const uint64_t u = a.lo + blockIdx.x;
-    const uint64_t ur = u - a.row0;  // row of u in the list / output arrays
-    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    double* P = reinterpret_cast<double*>(smem);             // k*k
-    double* csc = P + k * k;                                 // k
-    float* tile = reinterpret_cast<float*>(csc + k);         // k * kTileStride
-    uint32_t* cid = reinterpret_cast<uint32_t*>(tile + k * kTileStride);
-    uint32_t* det = cid + k;
-    uint32_t* order = det + k;   // rank -> candidate index
-    uint32_t* kp = order + k;    // kept ranked positions
-    uint32_t* rec = kp + k;      // recycled ids
-    uint32_t* kwset = rec + k;   // kept-keyword hash
-    uint32_t* ukw = kwset + a.kwcap;
-    __shared__ uint32_t nkept, nrec;
-
-    for (uint32_t j = tid; j < k; j += nt) {
-        cid[j] = a.L_ids[ur * k + j];
-        csc[j] = a.L_sc[ur * k + j];
-        P[j * k + j] = 0.0;
-    }
-    for (uint32_t j = tid; j < a.kwcap; j += nt) kwset[j] = kEmpty;
-    const uint64_t ub = a.c.kw_ptr[u], ue = a.c.kw_ptr[u + 1];
-    const uint32_t nukw = static_cast<uint32_t>(ue - ub);
-    for (uint32_t j = tid; j < nukw; j += nt) ukw[j] = a.c.kw_idx[ub + j];
-    __syncthreads();
-
-    // ---- candidate Gram (refine.cpp:11-23)
+// Generic (odd k) Gram: each thread owns up to kMaxPairsPerThread pairs.
+__device__ __forceinline__ void gram_pairs(const RefineArgs& a, uint32_t k, const uint32_t* cid, double* P,
+                                           float* tile) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
     const uint32_t npairs = k * (k - 1) / 2;
     for (uint32_t pbase = 0; pbase < npairs; pbase += nt * kMaxPairsPerThread) {
         double acc[kMaxPairsPerThread];
@@ -182,6 +161,124 @@ __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs 
             P[pi[q] * k + pj[q]] = s;
             P[pj[q] * k + pi[q]] = s;
         }
+    }
+}
+
+// Even k: the k candidates form k/2 row pairs; thread items are 2x2 blocks of
+// row pairs (bi < bj) plus the k/2 diagonal pairs (2m, 2m+1).  The dense rows
+// are staged TRANSPOSED as doubles (T[col][row], converted once at staging),
+// so one 16-B shared load yields a row pair and each element costs a thread
+// two loads for four DFMAs (the old lane-per-pair loop: two loads and two
+// F2F conversions per DFMA).  Every output is still its own sequential fp64
+// fma chain over the columns in order (= dense_dot, scoring.cpp:10-18).
+__device__ __forceinline__ void gram_blocked(const RefineArgs& a, uint32_t k, const uint32_t* cid, double* P,
+                                             double* T) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    const uint32_t kh = k >> 1, nblk = kh * (kh - 1) / 2;
+    const uint32_t S = k + 2;  // doubles per staged column (16-B aligned)
+    const double2* T2 = reinterpret_cast<const double2*>(T);
+    const uint32_t S2 = S >> 1;
+    const uint32_t rounds = max(1u, (nblk + 2 * nt - 1) / (2 * nt));
+    for (uint32_t rd = 0; rd < rounds; ++rd) {
+        uint32_t bi[2], bj[2];
+        bool bv[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t b = rd * 2 * nt + q * nt + tid;
+            bv[q] = b < nblk;
+            if (bv[q]) {
+                pair_of(b, kh, bi[q], bj[q]);
+            } else {
+                bi[q] = bj[q] = 0;
+            }
+        }
+        // diagonal pairs on the last threads of round 0
+        const bool sv = rd == 0 && tid >= nt - kh;  // kh <= nt (k <= 160: P fits the SM)
+        const uint32_t m = sv ? nt - 1 - tid : 0;
+        double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+        double accs = 0.0;
+        for (uint32_t d0 = 0; d0 < a.c.dstride; d0 += kTileD) {
+            const uint32_t w = min(kTileD, a.c.dstride - d0);  // multiple of 4
+            const uint32_t w4 = w >> 2;
+            for (uint32_t e = tid; e < k * w4; e += nt) {
+                const uint32_t r = e / w4, c4 = e % w4;
+                const float4 v = __ldg(reinterpret_cast<const float4*>(a.c.dense + (uint64_t)cid[r] * a.c.dstride + d0) + c4);
+                double* t = T + (size_t)(4 * c4) * S + r;
+                t[0] = (double)v.x;
+                t[S] = (double)v.y;
+                t[2 * S] = (double)v.z;
+                t[3 * S] = (double)v.w;
+            }
+            __syncthreads();
+            for (uint32_t c = 0; c < w; ++c) {
+                const double2* col = T2 + (size_t)c * S2;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double2 I = col[bi[q]], J = col[bj[q]];
+                    acc[q][0] = __fma_rn(I.x, J.x, acc[q][0]);
+                    acc[q][1] = __fma_rn(I.x, J.y, acc[q][1]);
+                    acc[q][2] = __fma_rn(I.y, J.x, acc[q][2]);
+                    acc[q][3] = __fma_rn(I.y, J.y, acc[q][3]);
+                }
+                const double2 M = col[m];
+                accs = __fma_rn(M.x, M.y, accs);
+            }
+            __syncthreads();
+        }
+        auto finish = [&](uint32_t i, uint32_t j, double s) {
+            const uint64_t x = cid[i], y = cid[j];
+            s = __dadd_rn(s, merge_dot(a.c.l_idx, a.c.l_val, a.c.l_off[x], a.c.l_nnz[x], a.c.l_off[y], a.c.l_nnz[y]));
+            s = __dadd_rn(s, merge_dot(a.c.s_idx, a.c.s_val, a.c.s_off[x], a.c.s_nnz[x], a.c.s_off[y], a.c.s_nnz[y]));
+            P[i * k + j] = s;
+            P[j * k + i] = s;
+        };
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (!bv[q]) continue;
+            const uint32_t i0 = 2 * bi[q], j0 = 2 * bj[q];
+            finish(i0, j0, acc[q][0]);
+            finish(i0, j0 + 1, acc[q][1]);
+            finish(i0 + 1, j0, acc[q][2]);
+            finish(i0 + 1, j0 + 1, acc[q][3]);
+        }
+        if (sv) finish(2 * m, 2 * m + 1, accs);
+    }
+}
+
+__global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t k = a.k;
+    const uint64_t u = a.lo + blockIdx.x;
+    const uint64_t ur = u - a.row0;  // row of u in the list / output arrays
+    const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    double* P = reinterpret_cast<double*>(smem);             // k*k
+    double* csc = P + k * k;                                 // k
+    float* tile = reinterpret_cast<float*>(csc + k);         // k * kTileStride
+    uint32_t* cid = reinterpret_cast<uint32_t*>(tile + tile_floats(k));
+    uint32_t* det = cid + k;
+    uint32_t* order = det + k;   // rank -> candidate index
+    uint32_t* kp = order + k;    // kept ranked positions
+    uint32_t* rec = kp + k;      // recycled ids
+    uint32_t* kwset = rec + k;   // kept-keyword hash
+    uint32_t* ukw = kwset + a.kwcap;
+    __shared__ uint32_t nkept, nrec;
+
+    for (uint32_t j = tid; j < k; j += nt) {
+        cid[j] = a.L_ids[ur * k + j];
+        csc[j] = a.L_sc[ur * k + j];
+        P[j * k + j] = 0.0;
+    }
+    for (uint32_t j = tid; j < a.kwcap; j += nt) kwset[j] = kEmpty;
+    const uint64_t ub = a.c.kw_ptr[u], ue = a.c.kw_ptr[u + 1];
+    const uint32_t nukw = static_cast<uint32_t>(ue - ub);
+    for (uint32_t j = tid; j < nukw; j += nt) ukw[j] = a.c.kw_idx[ub + j];
+    __syncthreads();
+
+    // ---- candidate Gram (refine.cpp:11-23)
+    if ((k & 1) == 0) {
+        gram_blocked(a, k, cid, P, reinterpret_cast<double*>(tile));
+    } else {
+        gram_pairs(a, k, cid, P, tile);
     }
     __syncthreads();
 
@@ -428,7 +525,7 @@ void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint6
     RefineArgs a{c.dc, k, degree, per_neighbour ? 1 : 0, g.ids.get(), g.scores.get(),
                  out.ordered.get(), out.ordered_sc.get(), out.detours.get(), out.kept.get(),
                  out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw, lo, row0};
-    const size_t sm = static_cast<size_t>(k) * k * 8 + k * 8 + static_cast<size_t>(k) * kTileStride * 4 +
+    const size_t sm = static_cast<size_t>(k) * k * 8 + k * 8 + static_cast<size_t>(tile_floats(k)) * 4 +
                       5 * k * 4 + static_cast<size_t>(kwcap) * 4 + static_cast<size_t>(max_kw) * 4 + 16;
     if (sm > 227 * 1024)
         throw Error("invalid-k", "refinery shared memory exceeds the SM (" + std::to_string(sm) + " B)");
