@@ -35,12 +35,21 @@ __host__ __device__ constexpr uint32_t tile_floats(uint32_t k) {
     return k * kTileStride > kTileD * (k + 2) * 2 ? k * kTileStride : kTileD * (k + 2) * 2;
 }
 
-// Sparse pair dot by merge-join (ascending term ids, matching products in
-// order).  Rows start on 4-posting boundaries and are padded with kPad, so
-// each side streams 16-B vectors with the next one already in flight: a
-// dependent global load every 4 steps instead of every step.
-__device__ __forceinline__ uint32_t lane4(const uint4& v, uint32_t i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+// Sparse pair dot by a block merge-join (ascending term ids, matching
+// products in order).  Rows start on 4-posting boundaries and are padded with
+// (kPad, 0), so each side is a sequence of 16-B blocks.  One step compares a
+// block of A with a block of B (16 compares), accumulates A's matches in lane
+// order, and advances the side whose last term is smaller (both when equal):
+// a match is found exactly once and the matched terms come out ascending, so
+// the fma chain is the merge_dot of scoring.cpp:24-74.  The step is branch-
+// free (selects and predicated loads), so the 32 lanes of a warp — each on its
+// own pair — stay converged; the element-wise merge this replaces diverged on
+// every step (70% of the kernel's stall samples at 200K docs).
+__device__ __forceinline__ void match4(uint32_t t, float vt, const uint4& b, const float4& vb, double& acc) {
+    const float sel = t == b.x ? vb.x : t == b.y ? vb.y : t == b.z ? vb.z : vb.w;
+    const bool hit = t != kPad && (t == b.x || t == b.y || t == b.z || t == b.w);
+    const double f = __fma_rn((double)vt, (double)sel, acc);
+    acc = hit ? f : acc;
 }
 
 __device__ double merge_dot(const uint32_t* idx, const float* val, uint64_t oa, uint32_t na,
@@ -49,37 +58,35 @@ __device__ double merge_dot(const uint32_t* idx, const float* val, uint64_t oa, 
     if (na == 0 || nb == 0) return acc;
     const uint4* A4 = reinterpret_cast<const uint4*>(idx + oa);
     const uint4* B4 = reinterpret_cast<const uint4*>(idx + ob);
+    const float4* VA = reinterpret_cast<const float4*>(val + oa);
+    const float4* VB = reinterpret_cast<const float4*>(val + ob);
     const uint32_t na4 = (na + 3) >> 2, nb4 = (nb + 3) >> 2;
-    const uint4 pad = make_uint4(kPad, kPad, kPad, kPad);
     uint4 ca = __ldg(A4), cb = __ldg(B4);
-    uint4 xa = na4 > 1 ? __ldg(A4 + 1) : pad, xb = nb4 > 1 ? __ldg(B4 + 1) : pad;
+    float4 cva = __ldg(VA), cvb = __ldg(VB);
     uint32_t i = 0, j = 0;
-    auto step_a = [&] {
-        ++i;
-        if ((i & 3) == 0) {
+    uint4 xa = __ldg(A4 + min(1u, na4 - 1)), xb = __ldg(B4 + min(1u, nb4 - 1));
+    float4 xva = __ldg(VA + min(1u, na4 - 1)), xvb = __ldg(VB + min(1u, nb4 - 1));
+    while (i < na4 && j < nb4) {
+        match4(ca.x, cva.x, cb, cvb, acc);
+        match4(ca.y, cva.y, cb, cvb, acc);
+        match4(ca.z, cva.z, cb, cvb, acc);
+        match4(ca.w, cva.w, cb, cvb, acc);
+        const bool adv_a = ca.w <= cb.w, adv_b = cb.w <= ca.w;
+        if (adv_a) {
+            ++i;
             ca = xa;
-            const uint32_t nx = (i >> 2) + 1;
-            xa = nx < na4 ? __ldg(A4 + nx) : pad;
+            cva = xva;
+            const uint32_t nx = min(i + 1, na4 - 1);
+            xa = __ldg(A4 + nx);
+            xva = __ldg(VA + nx);
         }
-    };
-    auto step_b = [&] {
-        ++j;
-        if ((j & 3) == 0) {
+        if (adv_b) {
+            ++j;
             cb = xb;
-            const uint32_t nx = (j >> 2) + 1;
-            xb = nx < nb4 ? __ldg(B4 + nx) : pad;
-        }
-    };
-    while (i < na && j < nb) {
-        const uint32_t a = lane4(ca, i & 3), b = lane4(cb, j & 3);
-        if (a < b) {
-            step_a();
-        } else if (b < a) {
-            step_b();
-        } else {
-            acc = __fma_rn((double)val[oa + i], (double)val[ob + j], acc);
-            step_a();
-            step_b();
+            cvb = xvb;
+            const uint32_t nx = min(j + 1, nb4 - 1);
+            xb = __ldg(B4 + nx);
+            xvb = __ldg(VB + nx);
         }
     }
     return acc;
@@ -152,14 +159,20 @@ __device__ __forceinline__ void gram_pairs(const RefineArgs& a, uint32_t k, cons
             __syncthreads();
         }
 #pragma unroll
+        for (int q = 0; q < kMaxPairsPerThread; ++q)
+            if (pi[q] != 0xFFFFFFFFu) P[pi[q] * k + pj[q]] = acc[q];
+#pragma unroll 1
         for (int q = 0; q < kMaxPairsPerThread; ++q) {
-            if (pi[q] == 0xFFFFFFFFu) continue;
-            const uint64_t x = cid[pi[q]], y = cid[pj[q]];
-            double s = acc[q];
+            const uint32_t p = pbase + q * nt + tid;
+            if (p >= npairs) continue;
+            uint32_t i, j;
+            pair_of(p, k, i, j);
+            const uint64_t x = cid[i], y = cid[j];
+            double s = P[i * k + j];
             s = __dadd_rn(s, merge_dot(a.c.l_idx, a.c.l_val, a.c.l_off[x], a.c.l_nnz[x], a.c.l_off[y], a.c.l_nnz[y]));
             s = __dadd_rn(s, merge_dot(a.c.s_idx, a.c.s_val, a.c.s_off[x], a.c.s_nnz[x], a.c.s_off[y], a.c.s_nnz[y]));
-            P[pi[q] * k + pj[q]] = s;
-            P[pj[q] * k + pi[q]] = s;
+            P[i * k + j] = s;
+            P[j * k + i] = s;
         }
     }
 }
@@ -210,6 +223,7 @@ __device__ __forceinline__ void gram_blocked(const RefineArgs& a, uint32_t k, co
                 t[3 * S] = (double)v.w;
             }
             __syncthreads();
+#pragma unroll 2
             for (uint32_t c = 0; c < w; ++c) {
                 const double2* col = T2 + (size_t)c * S2;
 #pragma unroll
@@ -225,23 +239,39 @@ __device__ __forceinline__ void gram_blocked(const RefineArgs& a, uint32_t k, co
             }
             __syncthreads();
         }
-        auto finish = [&](uint32_t i, uint32_t j, double s) {
-            const uint64_t x = cid[i], y = cid[j];
-            s = __dadd_rn(s, merge_dot(a.c.l_idx, a.c.l_val, a.c.l_off[x], a.c.l_nnz[x], a.c.l_off[y], a.c.l_nnz[y]));
-            s = __dadd_rn(s, merge_dot(a.c.s_idx, a.c.s_val, a.c.s_off[x], a.c.s_nnz[x], a.c.s_off[y], a.c.s_nnz[y]));
-            P[i * k + j] = s;
-            P[j * k + i] = s;
-        };
+        // park the dense sums in P (the thread owns these entries), so the
+        // sparse merges below do not keep nine fp64 accumulators live
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             if (!bv[q]) continue;
             const uint32_t i0 = 2 * bi[q], j0 = 2 * bj[q];
-            finish(i0, j0, acc[q][0]);
-            finish(i0, j0 + 1, acc[q][1]);
-            finish(i0 + 1, j0, acc[q][2]);
-            finish(i0 + 1, j0 + 1, acc[q][3]);
+            P[i0 * k + j0] = acc[q][0];
+            P[i0 * k + j0 + 1] = acc[q][1];
+            P[(i0 + 1) * k + j0] = acc[q][2];
+            P[(i0 + 1) * k + j0 + 1] = acc[q][3];
         }
-        if (sv) finish(2 * m, 2 * m + 1, accs);
+        if (sv) P[2 * m * k + 2 * m + 1] = accs;
+        auto finish = [&](uint32_t i, uint32_t j) {
+            const uint64_t x = cid[i], y = cid[j];
+            double s = P[i * k + j];
+#pragma unroll 1
+            for (int path = 0; path < 2; ++path) {  // dense + learned, then + statistical
+                const bool l = path == 0;
+                s = __dadd_rn(s, merge_dot(l ? a.c.l_idx : a.c.s_idx, l ? a.c.l_val : a.c.s_val,
+                                           l ? a.c.l_off[x] : a.c.s_off[x], l ? a.c.l_nnz[x] : a.c.s_nnz[x],
+                                           l ? a.c.l_off[y] : a.c.s_off[y], l ? a.c.l_nnz[y] : a.c.s_nnz[y]));
+            }
+            P[i * k + j] = s;
+            P[j * k + i] = s;
+        };
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+            if (!bv[q]) continue;
+            const uint32_t i0 = 2 * bi[q], j0 = 2 * bj[q];
+#pragma unroll 1
+            for (uint32_t e = 0; e < 4; ++e) finish(i0 + (e >> 1), j0 + (e & 1));
+        }
+        if (sv) finish(2 * m, 2 * m + 1);
     }
 }
 

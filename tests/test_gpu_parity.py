@@ -134,6 +134,25 @@ def test_refine_trace_identical(small, small_dev, small_ref, ref, per_neighbour)
     assert all(np.array_equal(a, b) for a, b in zip(gk, rk))
 
 
+@pytest.mark.parametrize("k", [15, 24, 64])
+def test_refine_shapes_identical(ref, k):
+    # odd k takes the pair-per-thread Gram, even k the 2x2-blocked one; dense
+    # dim 70 (stride 72: staged chunks of 32, 32, 8), sparse rows of 37 / 13
+    # postings (padded blocks) and a small vocabulary (long overlaps) for the
+    # block merge-join
+    p, c, kg, _ = corpus_of(docs=700, dense_dim=70, learned_vocab=400, learned_nnz=37,
+                            statistical_vocab=300, statistical_nnz=13, seed=11)
+    dev = fg.DeviceCorpus(c)
+    st = ref.store(c, kg)
+    lists = ref.knn_build(st, c.n, k, max_iterations=3, seed=42)
+    gs, gk, gt = fg.refine_graph(dev, *lists, degree=min(8, k - (k & 1)), trace=True)
+    rs, rk, rt = ref.refine(st, *lists, degree=min(8, k - (k & 1)), trace=True)
+    for key in ("ordered_ids", "detours", "kept_count"):
+        assert np.array_equal(gt[key], rt[key]), key
+    assert np.array_equal(gs, rs)
+    assert all(np.array_equal(a, b) for a, b in zip(gk, rk))
+
+
 @pytest.fixture(scope="module")
 def kg_case(ref):
     p, c, kg, chains = corpus_of(docs=1200, dense_dim=16, learned_vocab=2000, learned_nnz=16,

@@ -16,12 +16,13 @@ ap.add_argument("--queries", type=int, default=2000)
 ap.add_argument("--beam", type=int, default=256)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--entry", type=int, default=32)
+ap.add_argument("--svocab", type=int, default=0, help="statistical vocabulary (C3: 831592)")
 a = ap.parse_args()
 p = A.synth_params(docs=a.docs, dense_dim=768, learned_vocab=30522, learned_nnz=120,
-                   statistical_vocab=0, statistical_nnz=40, seed=1)
+                   statistical_vocab=a.svocab, statistical_nnz=40, seed=1)
 c, kg, _ = synth.generate_corpus(p, 0)
 dc = fg.DeviceCorpus(c)
-cache = f"/tmp/fgb_graph_{a.docs}_768_120_64_32.npz"
+cache = f"/tmp/fgb_graph_{a.docs}_768_120_{a.svocab}_64_32.npz"
 if os.path.exists(cache):
     z = np.load(cache)
     g = dict(degree=int(z["degree"]), semantic=z["semantic"], keyword=A.CSR(z["kp"], z["ki"]),
