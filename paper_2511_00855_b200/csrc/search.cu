@@ -1210,6 +1210,12 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.cap[1] = hash_capacity(up.max_snnz);
             pl.vocab[0] = bitmaps && c.l_vocab <= 65536 ? c.l_vocab : 0;
             pl.vocab[1] = bitmaps && c.s_vocab <= 65536 ? c.s_vocab : 0;
+            // one lookup mode per batch: when the batch walks both sparse
+            // paths and one needs the hash, both take it — running both
+            // modes' sparse groups overflows the instruction cache (C3 at 1M
+            // docs: 42.1K -> 44.6K QPS with the hash for both paths)
+            if (up.max_lnnz && up.max_snnz && (pl.vocab[0] == 0) != (pl.vocab[1] == 0))
+                pl.vocab[0] = pl.vocab[1] = 0;
             pl.beamcap = std::max(max_beam, 32u);
             pl.kcap = std::max(max_k, 1u);
             pl.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);

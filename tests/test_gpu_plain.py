@@ -70,6 +70,25 @@ def test_plain_c2_shape_identical(c2_small, ref, beam, entry):
         same(fg.batch_query(gix, q, entry_count=entry), g)
 
 
+def test_plain_c3_shape_identical(ref):
+    """configs[2] row shape: learned vocab 30,522 (bitmap-sized) + statistical
+    vocab 831,592 (hash-sized); the batch then takes the hash for both paths.
+    Per-query simplex weights over the three paths."""
+    p = A.synth_params(docs=3000, dense_dim=768, clusters=20, cluster_spread=0.25, learned_vocab=30522,
+                       learned_nnz=120, statistical_vocab=831592, statistical_nnz=40, seed=8)
+    c, kg, _ = synth.generate_corpus(p, 0)
+    dc = fg.DeviceCorpus(c)
+    gix = fg.build_hybrid_index(dc, kg, degree=16, knn_k=32, seed=42)
+    rix = ref.index_create(ref.store(c, kg), gix.export(), 32)
+    q = synth.synth_queries(p, 48, beam_width=128)
+    g = fg.batch_query(gix, q, entry_count=64)
+    same(g, ref.batch_query(rix, q, entry_count=64, threads=os.cpu_count() or 1))
+    # learned path alone (statistical weight 0): the learned bitmap again
+    q.weights[:, 2] = 0.0
+    same(fg.batch_query(gix, q, entry_count=64), ref.batch_query(rix, q, entry_count=64,
+                                                                  threads=os.cpu_count() or 1))
+
+
 def test_plain_forced_exact_resolution(c2_small, ref):
     """Error bound x1e9: nearly every comparison is 'uncertain' and resolved
     through the exact chain — results must not change."""
