@@ -41,6 +41,7 @@ ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
 ap.add_argument("--docs", type=int, default=0)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--eval-queries", type=int, default=1000)
+ap.add_argument("--max-beam", type=int, default=0, help="extend the beam sweep past 2048 (powers of two)")
 a = ap.parse_args()
 cfg = dict(CONFIGS[a.config])
 nq = cfg.pop("queries")
@@ -57,6 +58,9 @@ build_s = time.time() - t0
 queries = synth.synth_queries(p, nq)
 ev = queries.subset(np.arange(min(a.eval_queries, nq)))
 truth = fg.brute_force_topk(dc, ev)
+if a.max_beam:
+    while bench.BEAMS[-1] < a.max_beam:
+        bench.BEAMS.append(bench.BEAMS[-1] * 2)
 sweep = bench.sweep_operating_points(fg, ix, ev, truth, argparse.Namespace(entry=0, beam=0))
 best = bench.select_operating_point(sweep)
 q = queries.with_(beam_width=max(best["beam"], 10)).pinned()
