@@ -1212,9 +1212,13 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.vocab[1] = bitmaps && c.s_vocab <= 65536 ? c.s_vocab : 0;
             // one lookup mode per batch: when the batch walks both sparse
             // paths and one needs the hash, both take it — running both
-            // modes' sparse groups overflows the instruction cache (C3 at 1M
-            // docs: 42.1K -> 44.6K QPS with the hash for both paths)
-            if (up.max_lnnz && up.max_snnz && (pl.vocab[0] == 0) != (pl.vocab[1] == 0))
+            // modes' sparse groups overflows the instruction cache (C3/C4
+            // simplex batches at 1M docs: 41.6K -> 44.1K QPS).  Queries whose
+            // learned terms mostly hit (C4's chain queries without the hop
+            // reward) lose on the hash's probe loops: 79.3K -> 70.2K QPS
+            // (tools/mode_probe.py); FGB_SEARCH_MIXED=1 keeps both modes.
+            const char* me = std::getenv("FGB_SEARCH_MIXED");  // dev: keep both modes (A/B)
+            if (!(me && me[0] == '1') && up.max_lnnz && up.max_snnz && (pl.vocab[0] == 0) != (pl.vocab[1] == 0))
                 pl.vocab[0] = pl.vocab[1] = 0;
             pl.beamcap = std::max(max_beam, 32u);
             pl.kcap = std::max(max_k, 1u);
