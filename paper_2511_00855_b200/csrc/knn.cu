@@ -34,6 +34,7 @@ constexpr int kPassThreads = 512;
 // initial list quickly; later rounds amortise the merge's barriers).
 constexpr int kSRounds = 4;
 constexpr int kSCap = kSRounds * kPassThreads;  // entering candidates buffered per round
+constexpr uint32_t kSortMin = 32;  // entering batches above this size certify sorted
 
 // Rejection sampling (knn_graph.cpp:28-36) when 4k < n.
 __global__ void knn_sample_kernel(uint64_t n, uint32_t k, uint64_t seed, uint32_t* ids) {
@@ -254,6 +255,127 @@ __device__ void resolve_marked(const PassArgs& a, const SmemQuery& sq, uint8_t* 
         const uint32_t nf = min(total, capf);
         if (nf) exact_entries<NQ4>(a, sq, fixl, nf, area, area_bytes, T_sc, T_ex, T_id, S_sc, S_ex, S_id);
         if (total <= capf) break;
+    }
+    __syncthreads();
+}
+
+// #entries of the sorted list (sc, id)[0, n) that are better than (v, id)
+__device__ __forceinline__ uint32_t count_better(const double* sc, const uint32_t* id, uint32_t n, double v,
+                                                 uint32_t vid) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (better(sc[mid], id[mid], v, vid))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Sorted certification of a round's entering batch S (m > kSortMin) against
+// the list T (see the call site).  mrg: >= k + 1 words of scratch holding the
+// merged order's first k + 1 entries (bit 31: an S index, else a T index).
+template <int NQ4>
+__device__ void merge_certify_sorted(const PassArgs& a, const SmemQuery& sq, uint32_t m, uint32_t k, uint32_t n_c,
+                                     double eps, uint32_t* keys, uint32_t* fbits, double* T_sc, const uint32_t* T_id,
+                                     uint8_t* T_ex, uint8_t* T_mk, double* S_sc, uint32_t* S_id, uint8_t* S_ex,
+                                     uint8_t* S_mk, uint32_t* mrg, uint32_t* n_mark) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    __shared__ uint32_t any_mark;
+    const uint32_t p2 = 1u << (32 - __clz(m - 1));  // m <= kSCap, a power of two
+    auto certain = [&](double va, uint8_t ea, double vb, uint8_t eb) {
+        return (ea && eb) || fabs(va - vb) > 1.25 * ((ea ? 0.0 : eps) + (eb ? 0.0 : eps));
+    };
+    auto val = [&](uint32_t e) { return e >> 31 ? S_sc[e & 0x7FFFFFFFu] : T_sc[e]; };
+    auto ex = [&](uint32_t e) { return e >> 31 ? S_ex[e & 0x7FFFFFFFu] : T_ex[e]; };
+    auto mark = [&](uint32_t e) {
+        if (e >> 31) {
+            const uint32_t i = e & 0x7FFFFFFFu;
+            if (!S_ex[i]) {
+                S_mk[i] = 1;
+                any_mark = 1;
+            }
+        } else if (!T_ex[e]) {
+            T_mk[e] = 1;
+            any_mark = 1;
+        }
+    };
+    while (true) {
+        // bitonic sort of S[0, p2) by `better` on the stored values (padding
+        // entries are worse than every candidate and sort to the end)
+        for (uint32_t i = m + tid; i < p2; i += nt) {
+            S_sc[i] = -__longlong_as_double(0x7FF0000000000000LL);
+            S_id[i] = 0xFFFFFFFFu;
+            S_ex[i] = 1;
+        }
+        __syncthreads();
+        for (uint32_t size = 2; size <= p2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = tid; i < p2; i += nt) {
+                    const uint32_t j = i ^ stride;
+                    if (j <= i) continue;
+                    const bool first = (i & size) == 0;  // this half ends better-first
+                    const bool sw = first ? better(S_sc[j], S_id[j], S_sc[i], S_id[i])
+                                          : better(S_sc[i], S_id[i], S_sc[j], S_id[j]);
+                    if (sw) {
+                        const double ts = S_sc[i];
+                        S_sc[i] = S_sc[j];
+                        S_sc[j] = ts;
+                        const uint32_t ti = S_id[i];
+                        S_id[i] = S_id[j];
+                        S_id[j] = ti;
+                        const uint8_t te = S_ex[i];
+                        S_ex[i] = S_ex[j];
+                        S_ex[j] = te;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // merged positions of the first k + 1 entries
+        for (uint32_t i = tid; i < m; i += nt) {
+            const uint32_t pos = i + count_better(T_sc, T_id, k, S_sc[i], S_id[i]);
+            if (pos <= k) mrg[pos] = 0x80000000u | i;
+            S_mk[i] = 0;
+        }
+        for (uint32_t j = tid; j < k; j += nt) {
+            const uint32_t pos = j + count_better(S_sc, S_id, m, T_sc[j], T_id[j]);
+            if (pos <= k) mrg[pos] = j;
+            T_mk[j] = 0;
+        }
+        if (tid == 0) any_mark = 0;
+        __syncthreads();
+        // adjacent pairs inside the list: (p, p + 1), p + 1 < k
+        for (uint32_t p = tid; p + 1 < k; p += nt) {
+            const uint32_t x = mrg[p], y = mrg[p + 1];
+            if (!certain(val(x), ex(x), val(y), ex(y))) {
+                mark(x);
+                mark(y);
+            }
+        }
+        // the k-th entry against every entry merged below it
+        const uint32_t b = mrg[k - 1];
+        const double bv = val(b);
+        const uint8_t be = ex(b);
+        for (uint32_t i = tid; i < m; i += nt)
+            if (i + count_better(T_sc, T_id, k, S_sc[i], S_id[i]) >= k && !certain(bv, be, S_sc[i], S_ex[i])) {
+                mark(b);
+                mark(0x80000000u | i);
+            }
+        for (uint32_t j = tid; j < k; j += nt)
+            if (j + count_better(S_sc, S_id, m, T_sc[j], T_id[j]) >= k && !certain(bv, be, T_sc[j], T_ex[j])) {
+                mark(b);
+                mark(j);
+            }
+        __syncthreads();
+        if (!any_mark) break;
+        unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_c + 3) & ~3u));
+        const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_c + 3) & ~3u)) * 4;
+        resolve_marked<NQ4>(a, sq, S_mk, m, 0u, fbits, a.pool_cap / 16, n_mark, area, area_bytes, T_sc, T_ex, T_id,
+                            S_sc, S_ex, S_id);
+        resolve_marked<NQ4>(a, sq, T_mk, k, 0x80000000u, fbits, a.pool_cap / 16, n_mark, area, area_bytes, T_sc,
+                            T_ex, T_id, S_sc, S_ex, S_id);
     }
     __syncthreads();
 }
@@ -533,7 +655,23 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
             count(kKnRounds, 1);
         }
         if (m == 0) continue;
+        bool sorted = false;
         if constexpr (NQ4 > 0) {
+            if (m > kSortMin) {
+                // Large batches: sort S by its stored values, then certify
+                // only what the new top-k depends on — adjacent pairs of the
+                // merged order inside positions [0, k) (certified adjacent
+                // orders compose transitively into the true order) and the
+                // k-th entry against every entry merged below it.  O(m log^2 m
+                // + k) instead of O(m (k + m)), and pairs that both fall out
+                // of the list are never resolved.  Loops until nothing is
+                // uncertain (every round resolves at least one approximation).
+                sorted = true;
+                merge_certify_sorted<NQ4>(a, sq, m, k, n_c, eps, keys, fbits, T_sc, T_id, T_ex, T_mk, S_sc, S_id,
+                                          S_ex, S_mk, reinterpret_cast<uint32_t*>(T2_sc), &n_mark);
+            }
+        }
+        if constexpr (NQ4 > 0) if (!sorted) {
             // certify every comparison the rank-merge makes (S x T, S x S);
             // uncertain entries get the reference's exact score, until none is
             while (true) {
@@ -574,6 +712,27 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                                     T_sc, T_ex, T_id, S_sc, S_ex, S_id);
             }
         }
+        if (sorted) {
+            // both sorted: positions by binary search (ids are pairwise distinct)
+            for (uint32_t i = tid; i < k; i += nt) {
+                const uint32_t pos = i + count_better(S_sc, S_id, m, T_sc[i], T_id[i]);
+                if (pos < k) {
+                    T2_sc[pos] = T_sc[i];
+                    T2_id[pos] = T_id[i];
+                    T2_new[pos] = T_new[i];
+                    T2_ex[pos] = T_ex[i];
+                }
+            }
+            for (uint32_t i = tid; i < min(m, k); i += nt) {
+                const uint32_t pos = i + count_better(T_sc, T_id, k, S_sc[i], S_id[i]);
+                if (pos < k) {
+                    T2_sc[pos] = S_sc[i];
+                    T2_id[pos] = S_id[i];
+                    T2_new[pos] = 1;
+                    T2_ex[pos] = S_ex[i];
+                }
+            }
+        } else {
         // rank-merge T (sorted) with S (unsorted); ids are pairwise distinct
         for (uint32_t i = tid; i < k; i += nt) {
             uint32_t pos = i;
@@ -603,6 +762,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                 T2_new[pos] = 1;
                 T2_ex[pos] = S_ex[i];
             }
+        }
         }
         __syncthreads();
         for (uint32_t i = tid; i < k; i += nt) {
@@ -790,6 +950,10 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     const double u32 = std::ldexp(1.0, -24), u64 = std::ldexp(1.0, -53);
     a.eps32 = 4.0 * u32 / (1.0 - 4.0 * u32) * 1.01 + 1e-30;
     a.eps64 = (N + M + 8) * u64 * 1.01;
+    if (const char* e = std::getenv("FGB_KNN_EPS_SCALE")) {  // tests: force the exact resolutions
+        a.eps32 *= std::atof(e);
+        a.eps64 *= std::atof(e);
+    }
     a.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
     a.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
     a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;

@@ -100,6 +100,30 @@ def test_knn_init_and_pass_stagewise(small, small_dev, small_ref, ref, k):
         cur = r1[:3]
 
 
+@pytest.mark.parametrize("eps_scale", ["1", "1e6"])
+def test_knn_pass_k64_sorted_certification(ref, eps_scale):
+    # k = 64 on 2,500 docs: pass 1 enters hundreds of candidates per scoring
+    # round, so the sorted certification (entering batches > 32) runs; an
+    # error bound x1e6 forces its exact resolutions on most comparisons
+    import os
+    p, c, kg, _ = corpus_of(docs=2500, dense_dim=64, learned_vocab=3000, learned_nnz=24,
+                            statistical_vocab=3000, statistical_nnz=12, seed=13)
+    dev = fg.DeviceCorpus(c)
+    st = ref.store(c, kg)
+    cur = ref.knn_init(st, c.n, 64, 42)
+    threads = os.cpu_count() or 1
+    os.environ["FGB_KNN_EPS_SCALE"] = eps_scale
+    try:
+        for _ in range(3):
+            g1 = fg.nn_descent_iterate(dev, *cur)
+            r1 = ref.knn_iterate(st, *cur, threads=threads)
+            _same_lists(g1, r1)
+            assert g1[3] == r1[3]
+            cur = r1[:3]
+    finally:
+        os.environ.pop("FGB_KNN_EPS_SCALE", None)
+
+
 def test_knn_fisher_yates_branch(ref):
     # 4k >= n takes the partial Fisher-Yates path (knn_graph.cpp:37-46)
     p, c, kg, _ = corpus_of(docs=40, dense_dim=8, learned_vocab=50, learned_nnz=5,
