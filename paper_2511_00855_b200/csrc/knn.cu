@@ -34,7 +34,7 @@ constexpr int kPassThreads = 512;
 // initial list quickly; later rounds amortise the merge's barriers).
 constexpr int kSRounds = 4;
 constexpr int kSCap = kSRounds * kPassThreads;  // entering candidates buffered per round
-constexpr uint32_t kSortMin = 32;  // entering batches above this size certify sorted
+constexpr uint32_t kSortMin = 32;  // entering batches above this size certify sorted (default)
 
 // Rejection sampling (knn_graph.cpp:28-36) when 4k < n.
 __global__ void knn_sample_kernel(uint64_t n, uint32_t k, uint64_t seed, uint32_t* ids) {
@@ -133,6 +133,7 @@ struct PassArgs {
     // dev (FGB_KNN_TIMING=1): thread 0's cycles per phase + counters, summed
     unsigned long long* timing;
     int prefetch;       // L2 prefetch of the postings of the sparse groups after the first
+    uint32_t sort_min;  // entering batches larger than this certify sorted
 };
 
 enum : int {
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         if (m == 0) continue;
         bool sorted = false;
         if constexpr (NQ4 > 0) {
-            if (m > kSortMin) {
+            if (m > a.sort_min) {
                 // Large batches: sort S by its stored values, then certify
                 // only what the new top-k depends on — adjacent pairs of the
                 // merged order inside positions [0, k) (certified adjacent
@@ -929,7 +930,8 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0};
+               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin};
+    if (const char* e = std::getenv("FGB_KNN_SORT_MIN")) a.sort_min = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FGB_KNN_PREFETCH")) a.prefetch = std::atoi(e);
     DevBuf<unsigned long long> timing;
     const char* te = std::getenv("FGB_KNN_TIMING");
