@@ -886,11 +886,25 @@ void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s) {
     const uint32_t k = g.k;
     const uint64_t m = n * k;
     if (m >= 0xFFFFFFFFull) throw Error("invalid-argument", "n*k exceeds 2^32 entries");
-    DevBuf<uint64_t> keys_a(m), keys_b(m);
-    DevBuf<uint32_t> vals_a(m), vals_b(m), tkeys_a(m), tkeys_b(m), cnt(n), start(n);
-    R.ids.alloc(m);
-    R.cnt.alloc(n);
-    R.fresh.alloc(m);
+    auto& keys_a = R.keys_a;
+    auto& keys_b = R.keys_b;
+    auto& vals_a = R.vals_a;
+    auto& vals_b = R.vals_b;
+    auto& tkeys_a = R.tkeys_a;
+    auto& tkeys_b = R.tkeys_b;
+    auto& cnt = R.tcnt;
+    auto& start = R.tstart;
+    keys_a.ensure(m);
+    keys_b.ensure(m);
+    vals_a.ensure(m);
+    vals_b.ensure(m);
+    tkeys_a.ensure(m);
+    tkeys_b.ensure(m);
+    if (cnt.size() != n) cnt.alloc(n);  // zeroed whole below
+    start.ensure(n);
+    R.ids.ensure(m);
+    R.cnt.ensure(n);
+    R.fresh.ensure(m);
     cnt.zero(s);
     const unsigned gb = (unsigned)((m + 255) / 256);
     score_keys_kernel<<<gb, 256, 0, s>>>(g.scores.get(), m, keys_a.get(), vals_a.get());
@@ -903,7 +917,8 @@ void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s) {
     cub::DeviceRadixSort::SortPairs(nullptr, tb2, tkeys_a.get(), tkeys_b.get(), vals_b.get(),
                                     vals_a.get(), (int)m, 0, bits, s);
     cub::DeviceScan::ExclusiveSum(nullptr, tb3, cnt.get(), start.get(), (int)n, s);
-    DevBuf<unsigned char> temp(std::max({tb1, tb2, tb3, size_t(16)}));
+    DevBuf<unsigned char>& temp = R.temp;
+    temp.ensure(std::max({tb1, tb2, tb3, size_t(16)}));
     size_t tb = temp.size();
     FGB_CUDA(cub::DeviceRadixSort::SortPairsDescending(temp.get(), tb, keys_a.get(), keys_b.get(),
                                                        vals_a.get(), vals_b.get(), (int)m, 0, 64, s));
@@ -997,21 +1012,27 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     }
 }
 
-uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
-    ReverseLists R;
+uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s, ReverseLists& R, DevKnn& next,
+                            DevBuf<unsigned long long>& changed) {
     knn_reverse_lists(g, R, s);
-    DevKnn next;
-    next.alloc(g.n, g.k);
-    DevBuf<unsigned long long> changed(1);
+    if (next.n != g.n || next.k != g.k) next.alloc(g.n, g.k);
+    if (changed.size() != 1) changed.alloc(1);
     changed.zero(s);
     knn_pass_range(c, g, R, 0, g.n, next, changed.get(), s);
     unsigned long long h_changed = 0;
     changed.download(&h_changed, 1, s);
     FGB_CUDA(cudaStreamSynchronize(s));
-    g.ids = std::move(next.ids);
-    g.scores = std::move(next.scores);
-    g.fresh = std::move(next.fresh);
+    std::swap(g.ids, next.ids);  // the old snapshot's buffers serve the next pass
+    std::swap(g.scores, next.scores);
+    std::swap(g.fresh, next.fresh);
     return h_changed;
+}
+
+uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
+    ReverseLists R;
+    DevKnn next;
+    DevBuf<unsigned long long> changed;
+    return knn_iterate_device(c, g, s, R, next, changed);
 }
 
 uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
@@ -1021,8 +1042,11 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
     knn_init_device(c, k, seed, g, s);
     const double denom = static_cast<double>(c.n) * k;
     uint32_t passes = 0;
+    ReverseLists R;
+    DevKnn next;
+    DevBuf<unsigned long long> d_changed;
     for (uint32_t it = 0; it < max_iterations; ++it) {
-        const uint64_t changed = knn_iterate_device(c, g, s);
+        const uint64_t changed = knn_iterate_device(c, g, s, R, next, d_changed);
         ++passes;
         if (static_cast<double>(changed) / denom < convergence) break;
     }

@@ -26,6 +26,11 @@ struct ReverseLists {
     DevBuf<uint32_t> ids;    // n x k
     DevBuf<uint32_t> cnt;    // n
     DevBuf<uint8_t> fresh;   // n x k
+    // sort workspace, grow-only: a ReverseLists kept across passes allocates
+    // nothing after the first (each pass otherwise mapped and freed ~2 GB at 1M)
+    DevBuf<uint64_t> keys_a, keys_b;
+    DevBuf<uint32_t> vals_a, vals_b, tkeys_a, tkeys_b, tcnt, tstart;
+    DevBuf<unsigned char> temp;
 };
 
 // init_random_graph (knn_graph.cpp:52-73) into g (allocated n x k).
@@ -36,6 +41,9 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
                     DevKnn& next, unsigned long long* d_changed, cudaStream_t s);
 // nn_descent_iterate (knn_graph.cpp:75-148), in place; returns #replaced.
 uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s);
+// Same, reusing R / next / changed across passes (knn_build_device).
+uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s, ReverseLists& R, DevKnn& next,
+                            DevBuf<unsigned long long>& changed);
 // build_knn_graph (knn_graph.cpp:150-166); returns the number of passes run.
 uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
                           double convergence, uint64_t seed, DevKnn& g, cudaStream_t s);
