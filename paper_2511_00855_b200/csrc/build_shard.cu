@@ -135,11 +135,11 @@ void build_sharded(fg_index& ix, const fg_build_params& p, const Shards& sh, cud
     }
     const double denom = static_cast<double>(n) * k;
     DevBuf<unsigned long long> changed(1);
+    ReverseLists R;  // sort workspace and lists reused across passes
+    DevKnn next;
     for (uint32_t it = 0; it < p.knn_iterations; ++it) {
-        ReverseLists R;
         knn_reverse_lists(g, R, s);
-        DevKnn next;
-        alloc_padded(next, n, sh.n_pad, k);
+        if (it == 0) alloc_padded(next, n, sh.n_pad, k);
         changed.zero(s);
         for (int r : sh.mine) knn_pass_range(c, g, R, sh.lo(r), sh.hi(r), next, changed.get(), s);
         sh.gather(next.ids, k, s);
@@ -149,9 +149,9 @@ void build_sharded(fg_index& ix, const fg_build_params& p, const Shards& sh, cud
         unsigned long long h = 0;
         changed.download(&h, 1, s);
         FGB_CUDA(cudaStreamSynchronize(s));
-        g.ids = std::move(next.ids);
-        g.scores = std::move(next.scores);
-        g.fresh = std::move(next.fresh);
+        std::swap(g.ids, next.ids);  // the old snapshot's buffers serve the next pass
+        std::swap(g.scores, next.scores);
+        std::swap(g.fresh, next.fresh);
         if (static_cast<double>(h) / denom < 0.01) break;
     }
     ix.build_seconds[0] = secs(t0);
