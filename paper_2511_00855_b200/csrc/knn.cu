@@ -885,7 +885,8 @@ void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s) {
     const uint64_t n = g.n;
     const uint32_t k = g.k;
     const uint64_t m = n * k;
-    if (m >= 0xFFFFFFFFull) throw Error("invalid-argument", "n*k exceeds 2^32 entries");
+    // CUB's sorts/scans take int item counts
+    if (m >= 0x7FFFFFFFull) throw Error("invalid-argument", "n*k exceeds 2^31-1 list entries");
     auto& keys_a = R.keys_a;
     auto& keys_b = R.keys_b;
     auto& vals_a = R.vals_a;

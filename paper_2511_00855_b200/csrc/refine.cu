@@ -568,6 +568,10 @@ void refine_merge(uint64_t n, RefineOut& out, cudaStream_t s) {
     const uint32_t k = out.k, degree = out.degree;
     // ---- keepers sorted by (target, position, keeper) (refine.cpp:127-133)
     const uint64_t m = n * degree;
+    // CUB's sorts/scans take int item counts; keeper_keys_kernel packs the
+    // entry index in 32 bits
+    if (m >= 0x7FFFFFFFull || n >= 0x7FFFFFFFull)
+        throw Error("invalid-argument", "n*degree exceeds 2^31-1 edge entries");
     DevBuf<uint32_t> pos_a(m), pos_b(m), vals_a(m), vals_b(m), tkey_a(m), tkey_b(m), cnt(n + 1),
         start(n + 1);
     cnt.zero(s);

@@ -92,6 +92,8 @@ struct SearchArgs {
     uint32_t* r_warn;
     uint32_t* r_err;
     unsigned int* work;
+    const uint32_t* qlist;  // optional subset of query ids to run (overflow re-runs)
+    uint32_t qlist_n;
     // optional phase timing (FGB_SEARCH_TIMING=1): clock64 cycles summed over
     // warps per phase, see kPhase* below
     unsigned long long* timing;
@@ -487,18 +489,23 @@ __device__ bool has_relation(const SearchArgs& a, uint32_t x, uint32_t y) {
 }
 
 // Entity-context table (per warp, global memory): (node, ent, hop, has).
+// Probes are bounded by the capacity: a full table never spins.  The kernel
+// flags ERR_CTX once the load factor passes 1/2 and the host re-runs that
+// query with a larger table (fg_batch_query), so a -1 from ctx_slot only
+// occurs on a query whose result is discarded anyway.
 __device__ int ctx_find(const uint4* t, uint32_t cap, uint32_t node) {
     uint32_t s = hslot(node, cap - 1);
-    while (true) {
+    for (uint32_t probe = 0; probe < cap; ++probe) {
         const uint4 e = t[s];
         if (e.x == node) return static_cast<int>(s);
         if (e.x == kEmpty) return -1;
         s = (s + 1) & (cap - 1);
     }
+    return -1;
 }
 __device__ int ctx_slot(uint4* t, uint32_t cap, uint32_t node, uint32_t& used) {
     uint32_t s = hslot(node, cap - 1);
-    while (true) {
+    for (uint32_t probe = 0; probe < cap; ++probe) {
         const uint4 e = t[s];
         if (e.x == node) return static_cast<int>(s);
         if (e.x == kEmpty) {
@@ -508,6 +515,8 @@ __device__ int ctx_slot(uint4* t, uint32_t cap, uint32_t node, uint32_t& used) {
         }
         s = (s + 1) & (cap - 1);
     }
+    used = cap;  // full: the caller's load-factor test raises ERR_CTX
+    return -1;
 }
 
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs a) {
@@ -543,7 +552,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
         uint32_t qi = 0;
         if (lane == 0) qi = atomicAdd(a.work, 1u);
         qi = __shfl_sync(kFull, qi, 0);
-        if (qi >= a.q.count) break;
+        if (a.qlist) {  // re-run of the queries that overflowed their scratch
+            if (qi >= a.qlist_n) break;
+            qi = a.qlist[qi];
+        } else if (qi >= a.q.count) {
+            break;
+        }
         const uint32_t flags = a.qflags[qi];
         if (!(flags & QF_VALID)) {
             if (lane == 0) {
@@ -660,6 +674,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
         // assign_ctx (search.cpp:191-198), lane 0; returns true on change
         auto assign_ctx = [&](uint32_t node, uint32_t ent, uint32_t hop) {
             const int s = ctx_slot(ctx, a.ctxcap, node, ctx_used);
+            if (s < 0) return false;
             const uint4 e = ctx[s];
             if (e.w && (e.z < hop || (e.z == hop && e.y <= ent))) return false;
             ctx[s] = make_uint4(node, ent, hop, 1u);
@@ -1009,7 +1024,8 @@ constexpr uint64_t kId30 = 0x3FFFFFFFull;  // node ids must fit 30 bits in the p
 // Device results -> the caller's fg_search_results (ids -> doc ids, per-query
 // validation errors, counters); records the kernel time of ev0..ev1.
 void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg_search_results* out,
-                    const std::vector<std::string>& errs, uint64_t nq, uint32_t stride, cudaStream_t s) {
+                    std::vector<std::string>& errs, uint64_t nq, uint32_t stride, cudaStream_t s,
+                    double extra_ms = 0.0) {
     (void)q;
     SearchIo& io = ix->io;
     // pinned staging: 8-byte fields first, then the 4-byte ones
@@ -1033,10 +1049,12 @@ void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg
     FGB_CUDA(cudaStreamSynchronize(s));
     float ms = 0;
     FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
-    ix->last_kernel_ms = ms;
+    ix->last_kernel_ms = ms + extra_ms;
     for (uint64_t i = 0; i < nq; ++i) {
-        if (h_err[i])
-            throw Error("internal", "search scratch overflow (twin/context table) on query " + std::to_string(i));
+        // still overflowing after the re-runs at the largest scratch size:
+        // this query alone fails (batch_query's per-query capture, search.cpp:286-290)
+        if (h_err[i] && errs[i].empty())
+            errs[i] = "internal: search scratch overflow (twin pool / entity-context table)";
         const uint32_t cnt = errs[i].empty() ? h_count[i] : 0;
         out->hit_count[i] = cnt;
         for (uint32_t j = 0; j < cnt; ++j) {
@@ -1375,11 +1393,44 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(want_blocks, (uint64_t)sms * per_sm));
         const uint64_t slots = blocks * kWarpsPerBlock;
 
-        // ---- per-warp scratch (reused across calls)
+        // ---- per-warp scratch (reused across calls).  The twin pool and the
+        // entity-context table start at 8,192 slots (the context table at
+        // least 4x the largest seed set); a query that overflows them is
+        // re-run alone with 4x larger tables (up to kMaxScratch), so only a
+        // query that still overflows there fails, through its own error.
         a.nwords = (n + 31) / 32;
         a.tcap = 16384;
-        a.twcap = any_req ? 8192 : 0;
-        a.ctxcap = any_ctx ? 8192 : 0;
+        uint32_t twcap0 = any_req ? 8192 : 0, ctxcap0 = 0;
+        if (any_ctx) {
+            ctxcap0 = 8192;
+            while (ctxcap0 < 4ull * max_seeds && ctxcap0 < (1u << 26)) ctxcap0 <<= 1;
+        }
+        if (const char* e = std::getenv("FGB_SEARCH_SCRATCH0")) {  // test hook: force re-runs
+            const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+            if (v >= 16 && (v & (v - 1)) == 0) {
+                if (any_req) twcap0 = v;
+                if (any_ctx) ctxcap0 = v;
+            }
+        }
+        float ms_prev = 0.f;
+        std::vector<uint32_t> rerun;
+        DevBuf<uint32_t> d_rerun;
+        DevBuf<unsigned long long> timing;
+        const char* te = std::getenv("FGB_SEARCH_TIMING");
+        if (te && te[0] == '1') {
+            timing.alloc(kPhCount);
+            timing.zero(s);
+            a.timing = timing.get();
+        }
+        a.prefetch = 1;
+        if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) a.prefetch = std::atoi(e);
+        const uint64_t all_blocks = blocks;
+        for (int attempt = 0;; ++attempt) {
+        a.twcap = twcap0 << (2 * attempt);
+        a.ctxcap = ctxcap0 << (2 * attempt);
+        // a re-run needs one query-warp per overflowed query at most
+        const uint64_t blocks = attempt ? std::min<uint64_t>(all_blocks, rerun.size()) : all_blocks;
+        const uint64_t slots = blocks * kWarpsPerBlock;
         const uint64_t nbitsets = 1 + (any_ctx ? 1 : 0) + (any_req ? 1 : 0);
         const uint64_t bits_words = slots * a.nwords * nbitsets;
         if (ix->scratch_bits.size() < bits_words) {
@@ -1408,23 +1459,32 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         a.r_warn = r_warn.get();
         a.r_err = r_err.get();
         a.work = work.get();
-
-        a.prefetch = 1;
-        if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) a.prefetch = std::atoi(e);
-        DevBuf<unsigned long long> timing;
-        const char* te = std::getenv("FGB_SEARCH_TIMING");
-        if (te && te[0] == '1') {
-            timing.alloc(kPhCount);
-            timing.zero(s);
-            a.timing = timing.get();
-        }
+        a.qlist = attempt ? d_rerun.get() : nullptr;
+        a.qlist_n = static_cast<uint32_t>(rerun.size());
+        if (attempt) FGB_CUDA(cudaMemsetAsync(work.get(), 0, sizeof(unsigned int), s));
         FGB_CUDA(cudaEventRecord(ix->ev0, s));
         if (nq) search_kernel<<<(unsigned)blocks, kWarpsPerBlock * 32, block_smem, s>>>(a);
         FGB_LAUNCH("search_kernel");
         FGB_CUDA(cudaEventRecord(ix->ev1, s));
+        ix->last_launches = nq ? attempt + 1 : 0;
+        // overflowed queries: re-run them alone with larger scratch
+        constexpr uint64_t kMaxScratch = 1ull << 30;  // bytes of twin + context tables per launch
+        std::vector<uint32_t> h_err(nq);
+        if (nq) r_err.download(h_err.data(), nq, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        rerun.clear();
+        for (uint64_t i = 0; i < nq; ++i)
+            if (h_err[i]) rerun.push_back(static_cast<uint32_t>(i));
+        const uint64_t next_slots = std::min<uint64_t>(all_blocks, rerun.size()) * kWarpsPerBlock;
+        const uint64_t next_bytes = next_slots * ((uint64_t(a.twcap) * 12 + uint64_t(a.ctxcap) * 16) << 2);
+        if (rerun.empty() || next_bytes > kMaxScratch) break;
+        float ms = 0;
+        FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
+        ms_prev += ms;
+        d_rerun.upload(rerun, s);
+        }  // attempts
 
-        finish_results(ix, c, q, out, errs, nq, stride, s);
-        ix->last_launches = nq ? 1 : 0;
+        finish_results(ix, c, q, out, errs, nq, stride, s, ms_prev);
         if (a.timing) {
             unsigned long long t[kPhCount];
             timing.download(t, kPhCount, s);
@@ -1433,7 +1493,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             static const char* names[] = {"seeds", "select", "adjacency", "dedupe+visited", "score",
                                           "merge", "final"};
             std::fprintf(stderr, "[search timing] %llu queries, %.1f expansions/query, %d warps, %.3f ms\n",
-                         t[kPhQueries], X / std::max(1ull, t[kPhQueries]), (int)slots, ix->last_kernel_ms);
+                         t[kPhQueries], X / std::max(1ull, t[kPhQueries]), (int)all_blocks, ix->last_kernel_ms);
             for (int k = 0; k < kPhLaneSparse; ++k)
                 std::fprintf(stderr, "  %-15s %10.0f cycles/expansion\n", names[k], t[k] / X);
             std::fprintf(stderr, "  lane: sparse %.0f cycles/node, dense %.0f cycles/node, scored %llu, dense rows %llu\n",

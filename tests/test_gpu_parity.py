@@ -286,3 +286,27 @@ def test_brute_force_identical(kg_case, ref):
     g = fg.brute_force_topk(dev, q)
     r = ref.index_brute_force(rix, q)
     _same_results(g, r, check_expanded=False)
+
+
+def test_search_scratch_overflow_reruns(kg_case, ref, monkeypatch):
+    # a query that overflows the twin pool / entity-context table
+    # must neither hang nor fail the batch.  A 16-slot initial table forces
+    # the overflow path on most queries; the library re-runs them alone with
+    # larger tables and the results stay identical to the reference's.
+    p, c, kg, chains, dev, gix, rix = kg_case
+    monkeypatch.setenv("FGB_SEARCH_SCRATCH0", "16")
+    dense = np.stack([ch.query_dense for ch in chains])
+    lr = [ch.query_learned for ch in chains]
+    sr = [ch.query_statistical for ch in chains]
+    learned = A.CSR.from_rows([x[0] for x in lr], [x[1] for x in lr])
+    stat = A.CSR.from_rows([x[0] for x in sr], [x[1] for x in sr])
+    w = np.tile(np.array([[1, 1, 1, 100]], np.float32), (len(chains), 1))
+    ents = A.CSR.from_rows([[ch.e0] for ch in chains])
+    q = A.Queries(dense, learned, stat, w, k=10, beam_width=64, max_entity_hops=2, entities=ents)
+    g = fg.batch_query(gix, q)
+    assert gix.last_search_stats()[1] >= 2  # the overflow re-run happened
+    _same_results(g, ref.batch_query(rix, q))
+    q = synth.synth_queries(p, 30, beam_width=200)
+    q.required = A.CSR.from_rows([q.statistical.row(i)[0][:1].tolist() for i in range(q.count)])
+    for conj in (True, False):
+        _same_results(fg.batch_query(gix, q, conjunctive=conj), ref.batch_query(rix, q, conjunctive=conj))
