@@ -13,9 +13,17 @@
 //   search.hpp:84    search              -> fg_batch_query (one row)
 //   search.hpp:86    batch_query         -> fg_batch_query
 //   eval.hpp:20      brute_force_topk    -> fg_brute_force_topk
+//   update.hpp:33    insert_batch        -> fg_index_insert (device mirror updated in place)
+//   update.hpp:38    mark_delete         -> fg_corpus_set_deleted (device mirror updated in place)
+//
+// Device mirrors (corpus + index) are cached by an O(1) key (see Mirrors)
+// and reused across calls: batch_scores / knn / refine / brute force reuse
+// the uploaded corpus, searches on an index returned by build_hybrid_index
+// reuse the build's own device index.
 //
 // Errors come back as fusegraph::Error with the reference's codes.
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -23,6 +31,7 @@
 #include <vector>
 
 #include "fg_b200.h"
+#include "fusegraph/corpus.hpp"
 #include "fusegraph/eval.hpp"
 #include "fusegraph/index.hpp"
 #include "fusegraph/knn_graph.hpp"
@@ -30,6 +39,8 @@
 #include "fusegraph/refine.hpp"
 #include "fusegraph/scoring.hpp"
 #include "fusegraph/search.hpp"
+#include "fusegraph/update.hpp"
+#include "fusegraph_b200_shim.hpp"
 
 namespace fusegraph {
 namespace {
@@ -93,6 +104,138 @@ struct Corpus {  // RAII device corpus
     }
     ~Corpus() { fg_corpus_free(h); }
 };
+
+// O(1) identity of a DocumentStore / HybridIndex: the heap buffers of its
+// tables (they survive moves, so an index returned by value keeps its key)
+// plus a checksum of a fixed sample of 64 nodes.  The reference declares a
+// built index immutable except through the maintenance API (index.hpp:33),
+// and insert_batch / mark_delete below update the device mirror in place,
+// so no per-call O(n) walk is needed; the sample catches a destroyed index
+// whose buffers were reused by a new one.  Code that edits the structs
+// directly calls fusegraph::b200::invalidate_device_mirrors().
+uint64_t mix(uint64_t h, uint64_t v) { return (h ^ v) * 1099511628211ull; }
+uint64_t bits_of(double d) {
+    uint64_t b;
+    std::memcpy(&b, &d, 8);
+    return b;
+}
+uint64_t store_sample(const DocumentStore& st) {
+    uint64_t h = mix(1469598103934665603ull, st.size());
+    h = mix(h, st.dense_dim);
+    const std::size_t n = st.size();
+    for (std::size_t i = 0; i < 64 && n; ++i) {
+        const auto& d = st.docs[(i * 0x9E3779B97F4A7C15ull) % n];
+        h = mix(h, d.doc_id);
+        h = mix(h, d.deleted);
+        h = mix(h, bits_of(d.vector.squared_norm));
+        h = mix(h, d.vector.learned.indices.size() + (d.vector.statistical.indices.size() << 20));
+    }
+    return h;
+}
+struct StoreKey {
+    const void* docs = nullptr;
+    std::size_t n = 0;
+    uint64_t sample = 0;
+    bool operator==(const StoreKey&) const = default;
+};
+StoreKey store_key(const DocumentStore& st) { return {st.docs.data(), st.size(), store_sample(st)}; }
+
+struct IndexKey {
+    StoreKey store;
+    const void* semantic = nullptr;
+    const void* norm = nullptr;
+    uint64_t sample = 0;
+    bool operator==(const IndexKey&) const = default;
+};
+IndexKey index_key(const HybridIndex& x) {
+    uint64_t h = mix(1469598103934665603ull, x.degree);
+    h = mix(h, x.kg.triplets().size());
+    const std::size_t n = x.size();
+    for (std::size_t i = 0; i < 64 && n && x.semantic.size() == n; ++i) {
+        const std::size_t u = (i * 0x9E3779B97F4A7C15ull) % n;
+        for (uint32_t v : x.semantic[u]) h = mix(h, v);
+        h = mix(h, x.keyword[u].size());
+        h = mix(h, x.logical[u].size());
+        h = mix(h, x.norm_order.size() == n ? x.norm_order[u] : ~0ull);
+    }
+    return {store_key(x.store), x.semantic.data(), x.norm_order.data(), h};
+}
+
+// Device mirrors, most recent first (two of each: a 1M-doc mirror is ~5 GB).
+struct Mirrors {
+    std::mutex mu;
+    struct C {
+        StoreKey key;
+        std::shared_ptr<Corpus> corpus;
+    };
+    struct I {
+        IndexKey key;
+        std::shared_ptr<Corpus> corpus;
+        fg_index* ix = nullptr;
+    };
+    std::vector<C> corpora;
+    std::vector<I> indexes;
+    static constexpr std::size_t kKeep = 2;
+
+    ~Mirrors() { clear(); }
+    void clear() {
+        for (auto& e : indexes) fg_index_free(e.ix);
+        indexes.clear();
+        corpora.clear();
+    }
+    std::shared_ptr<Corpus> corpus(const DocumentStore& st) {
+        const StoreKey k = store_key(st);
+        for (std::size_t i = 0; i < corpora.size(); ++i)
+            if (corpora[i].key == k) {
+                std::rotate(corpora.begin(), corpora.begin() + i, corpora.begin() + i + 1);
+                return corpora[0].corpus;
+            }
+        for (auto& e : indexes)  // an index mirror's corpus serves its store
+            if (e.key.store == k) return remember(k, e.corpus);
+        return remember(k, std::make_shared<Corpus>(st));
+    }
+    std::shared_ptr<Corpus> remember(const StoreKey& k, std::shared_ptr<Corpus> c) {
+        corpora.insert(corpora.begin(), {k, c});
+        if (corpora.size() > kKeep) corpora.pop_back();
+        return c;
+    }
+    void adopt(const IndexKey& k, std::shared_ptr<Corpus> c, fg_index* ix) {
+        indexes.insert(indexes.begin(), {k, std::move(c), ix});
+        if (indexes.size() > kKeep) {
+            fg_index_free(indexes.back().ix);
+            indexes.pop_back();
+        }
+    }
+    I* find(const IndexKey& k) {
+        for (std::size_t i = 0; i < indexes.size(); ++i)
+            if (indexes[i].key == k) {
+                std::rotate(indexes.begin(), indexes.begin() + i, indexes.begin() + i + 1);
+                return &indexes[0];
+            }
+        return nullptr;
+    }
+    fg_index* index(const HybridIndex& x);
+    // the struct changed through the maintenance API and the mirror `ix`
+    // was updated to match: re-key it (and its corpus) to the new content
+    void rekey(fg_index* ix, const IndexKey& k) {
+        for (auto& e : indexes)
+            if (e.ix == ix) {
+                for (auto& c : corpora)
+                    if (c.corpus == e.corpus) c.key = k.store;
+                e.key = k;
+            }
+    }
+    // mark_delete: push the deleted flags to the mirror of the index (if any)
+    void set_deleted(const IndexKey& before, const HybridIndex& x) {
+        I* e = find(before);
+        if (!e) return;
+        std::vector<uint8_t> flags(x.size());
+        for (std::size_t u = 0; u < x.size(); ++u) flags[u] = x.store.docs[u].deleted ? 1 : 0;
+        ok(fg_corpus_set_deleted(e->corpus->h, flags.data()));
+        rekey(e->ix, index_key(x));
+    }
+};
+Mirrors g_mirrors;
 
 struct KgFlat {
     std::vector<uint32_t> s, r, t;
@@ -162,52 +305,29 @@ KnnGraph to_graph(uint64_t n, uint32_t k, const std::vector<uint32_t>& ids,
     return g;
 }
 
-// Device mirror of a HybridIndex, cached by identity + a content fingerprint
-// (mark_delete / insert_batch mutate the struct in place).
-struct IndexCache {
-    std::mutex mu;
-    const HybridIndex* key = nullptr;
-    uint64_t fp = 0;
-    std::unique_ptr<Corpus> corpus;
+// Device mirror of a HybridIndex: found by key, else uploaded from the host
+// struct (its corpus mirror reused when the store is already on the device).
+fg_index* Mirrors::index(const HybridIndex& x) {
+    const IndexKey k = index_key(x);
+    if (I* e = find(k)) return e->ix;
+    auto c = corpus(x.store);
+    const uint64_t n = x.size();
+    std::vector<uint32_t> sem(n * x.degree), ki, lg, norm(x.norm_order);
+    std::vector<uint64_t> kp{0}, lp{0};
+    for (uint64_t u = 0; u < n; ++u) {
+        std::copy(x.semantic[u].begin(), x.semantic[u].end(), sem.begin() + u * x.degree);
+        ki.insert(ki.end(), x.keyword[u].begin(), x.keyword[u].end());
+        kp.push_back(ki.size());
+        for (const auto& e : x.logical[u]) lg.insert(lg.end(), {e.source, e.relation, e.target, e.via});
+        lp.push_back(lg.size() / 4);
+    }
+    KgFlat kg(x.kg);
+    fg_graph_view gv{x.degree, sem.data(), {kp.data(), ki.data()}, lp.data(), lg.data(), norm.data()};
     fg_index* ix = nullptr;
-
-    static uint64_t fingerprint(const HybridIndex& x) {
-        uint64_t h = 1469598103934665603ull ^ x.size();
-        auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
-        for (std::size_t u = 0; u < x.size(); ++u) {
-            mix(x.store.docs[u].deleted);
-            mix(x.semantic[u].empty() ? ~0u : x.semantic[u][0]);
-            mix(x.keyword[u].size());
-            mix(x.logical[u].size());
-        }
-        return h;
-    }
-
-    fg_index* get(const HybridIndex& x) {
-        const uint64_t f = fingerprint(x);
-        if (ix && key == &x && fp == f) return ix;
-        if (ix) fg_index_free(ix);
-        ix = nullptr;
-        corpus = std::make_unique<Corpus>(x.store);
-        const uint64_t n = x.size();
-        std::vector<uint32_t> sem(n * x.degree), ki, lg, norm(x.norm_order);
-        std::vector<uint64_t> kp{0}, lp{0};
-        for (uint64_t u = 0; u < n; ++u) {
-            std::copy(x.semantic[u].begin(), x.semantic[u].end(), sem.begin() + u * x.degree);
-            ki.insert(ki.end(), x.keyword[u].begin(), x.keyword[u].end());
-            kp.push_back(ki.size());
-            for (const auto& e : x.logical[u]) lg.insert(lg.end(), {e.source, e.relation, e.target, e.via});
-            lp.push_back(lg.size() / 4);
-        }
-        KgFlat kg(x.kg);
-        fg_graph_view gv{x.degree, sem.data(), {kp.data(), ki.data()}, lp.data(), lg.data(), norm.data()};
-        ok(fg_index_create(corpus->h, &kg.v, &gv, &ix));
-        key = &x;
-        fp = f;
-        return ix;
-    }
-};
-IndexCache g_cache;
+    ok(fg_index_create(c->h, &kg.v, &gv, &ix));
+    adopt(k, c, ix);
+    return ix;
+}
 
 std::vector<SearchResult> run_gpu(const HybridIndex& index, std::span<const QuerySpec> queries,
                                   const SearchOptions& opts);
@@ -242,8 +362,8 @@ std::vector<SearchResult> run_gpu(const HybridIndex& index, std::span<const Quer
                                   const SearchOptions& opts) {
     std::vector<SearchResult> out(queries.size());
     if (queries.empty()) return out;
-    std::lock_guard<std::mutex> lock(g_cache.mu);
-    fg_index* ix = g_cache.get(index);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    fg_index* ix = g_mirrors.index(index);
     QueryFlat qf(queries);
     uint32_t kmax = 1;
     for (const auto& q : queries) kmax = std::max(kmax, q.k);
@@ -275,30 +395,33 @@ std::vector<Score> batch_scores(const FusedVector& weighted_query, std::span<con
     for (uint32_t id : ids) (void)store.doc(id);  // unknown-id, like store.doc()
     std::vector<Score> out(ids.size());
     if (ids.empty()) return out;
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     QuerySpec q;
     q.vector = weighted_query;  // already weighted: unit weights keep it as is
     QueryFlat qf(std::span<const QuerySpec>(&q, 1));
     if (qf.v.dense_dim != store.dense_dim && store.size())
         throw Error("dim-mismatch", "dense dimensions differ: " + std::to_string(qf.v.dense_dim) +
                                         " vs " + std::to_string(store.docs[0].vector.dense.dim()));
-    ok(fg_batch_scores(c.h, &qf.v, 0, ids.data(), ids.size(), out.data()));
+    ok(fg_batch_scores(c->h, &qf.v, 0, ids.data(), ids.size(), out.data()));
     return out;
 }
 
 KnnGraph init_random_graph(const DocumentStore& store, uint32_t k, uint64_t seed, unsigned) {
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     const uint64_t n = store.size();
     std::vector<uint32_t> ids(n * k);
     std::vector<double> sc(n * k);
     std::vector<uint8_t> fr(n * k);
     fg_knn_lists l{n, k, ids.data(), sc.data(), fr.data()};
-    ok(fg_knn_init(c.h, k, seed, &l));
+    ok(fg_knn_init(c->h, k, seed, &l));
     return to_graph(n, k, ids, sc, fr);
 }
 
 std::size_t nn_descent_iterate(const DocumentStore& store, KnnGraph& graph, unsigned) {
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     const uint64_t n = graph.size();
     const uint32_t k = graph.k;
     std::vector<uint32_t> ids(n * k);
@@ -312,13 +435,14 @@ std::size_t nn_descent_iterate(const DocumentStore& store, KnnGraph& graph, unsi
         }
     fg_knn_lists l{n, k, ids.data(), sc.data(), fr.data()};
     uint64_t changed = 0;
-    ok(fg_knn_iterate(c.h, &l, &changed));
+    ok(fg_knn_iterate(c->h, &l, &changed));
     graph = to_graph(n, k, ids, sc, fr);
     return changed;
 }
 
 KnnGraph build_knn_graph(const DocumentStore& store, const KnnBuildParams& p) {
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     const uint64_t n = store.size();
     const uint32_t kk = (n >= 2 && p.k >= n) ? static_cast<uint32_t>(n - 1) : p.k;
     std::vector<uint32_t> ids(n * kk);
@@ -326,13 +450,14 @@ KnnGraph build_knn_graph(const DocumentStore& store, const KnnBuildParams& p) {
     std::vector<uint8_t> fr(n * kk);
     fg_knn_lists l{n, kk, ids.data(), sc.data(), fr.data()};
     fg_knn_params kp{p.k, p.max_iterations, p.convergence, p.seed};
-    ok(fg_knn_build(c.h, &kp, &l, nullptr));
+    ok(fg_knn_build(c->h, &kp, &l, nullptr));
     return to_graph(n, l.k, ids, sc, fr);
 }
 
 RefinedEdges refine_graph(const DocumentStore& store, const KnnGraph& knn, const RefineParams& p,
                           RefineTrace* trace) {
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     const uint64_t n = knn.size();
     const uint32_t k = knn.k;
     std::vector<uint32_t> ids(n * k);
@@ -351,7 +476,7 @@ RefinedEdges refine_graph(const DocumentStore& store, const KnnGraph& knn, const
     fg_refined out{sem.data(), k, kw.data(), kwc.data()};
     fg_refine_trace tr{oid.data(), osc.data(), det.data(), kept.data(), keptc.data()};
     fg_refine_params rp{p.degree, p.per_neighbour_keyword_check ? 1 : 0};
-    ok(fg_refine(c.h, &l, &rp, &out, trace ? &tr : nullptr));
+    ok(fg_refine(c->h, &l, &rp, &out, trace ? &tr : nullptr));
     RefinedEdges e;
     e.semantic.resize(n);
     e.keyword.resize(n);
@@ -372,6 +497,29 @@ RefinedEdges refine_graph(const DocumentStore& store, const KnnGraph& knn, const
     }
     return e;
 }
+
+namespace {
+// Host copies of the device index's edge tables into the reference struct.
+void pull_edges(fg_index* ix, HybridIndex& index, uint64_t nn) {
+    uint32_t deg = 0;
+    uint64_t kt = 0, lt = 0;
+    ok(fg_index_sizes(ix, &deg, &kt, &lt));
+    std::vector<uint32_t> sem(nn * deg), ki(kt), lg(lt * 4), norm(nn);
+    std::vector<uint64_t> kp(nn + 1), lp(nn + 1);
+    ok(fg_index_export(ix, sem.data(), kp.data(), ki.data(), lp.data(), lg.data(), norm.data()));
+    index.semantic.resize(nn);
+    index.keyword.resize(nn);
+    index.logical.resize(nn);
+    for (uint64_t u = 0; u < nn; ++u) {
+        index.semantic[u].assign(sem.begin() + u * deg, sem.begin() + (u + 1) * deg);
+        index.keyword[u].assign(ki.begin() + kp[u], ki.begin() + kp[u + 1]);
+        index.logical[u].clear();
+        for (uint64_t e = lp[u]; e < lp[u + 1]; ++e)
+            index.logical[u].push_back({lg[4 * e], lg[4 * e + 1], lg[4 * e + 2], lg[4 * e + 3]});
+    }
+    index.norm_order = std::move(norm);
+}
+}  // namespace
 
 HybridIndex build_hybrid_index(DocumentStore store, KnowledgeGraph kg, const BuildParams& params,
                                RefineTrace* trace) {
@@ -408,33 +556,24 @@ HybridIndex build_hybrid_index(DocumentStore store, KnowledgeGraph kg, const Bui
         rebuild_norm_order(index);
         return index;
     }
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     KgFlat kf(kg);
     fg_build_params bp{params.degree, params.knn_k, params.knn_iterations, params.seed,
                        params.logical_cap, params.default_entity_hops,
                        params.per_neighbour_keyword_check ? 1 : 0};
     fg_index* ix = nullptr;
-    ok(fg_index_build(c.h, &kf.v, &bp, &ix));
-    uint32_t deg = 0;
-    uint64_t kt = 0, lt = 0;
-    ok(fg_index_sizes(ix, &deg, &kt, &lt));
-    std::vector<uint32_t> sem(n * deg), ki(kt), lg(lt * 4), norm(n);
-    std::vector<uint64_t> kp(n + 1), lp(n + 1);
-    ok(fg_index_export(ix, sem.data(), kp.data(), ki.data(), lp.data(), lg.data(), norm.data()));
-    fg_index_free(ix);
-    index.semantic.resize(n);
-    index.keyword.resize(n);
-    index.logical.resize(n);
-    for (uint64_t u = 0; u < n; ++u) {
-        index.semantic[u].assign(sem.begin() + u * deg, sem.begin() + (u + 1) * deg);
-        index.keyword[u].assign(ki.begin() + kp[u], ki.begin() + kp[u + 1]);
-        for (uint64_t e = lp[u]; e < lp[u + 1]; ++e)
-            index.logical[u].push_back({lg[4 * e], lg[4 * e + 1], lg[4 * e + 2], lg[4 * e + 3]});
+    ok(fg_index_build(c->h, &kf.v, &bp, &ix));
+    try {
+        pull_edges(ix, index, n);
+    } catch (...) {
+        fg_index_free(ix);
+        throw;
     }
-    index.norm_order = std::move(norm);
-    index.store = std::move(store);
+    index.store = std::move(store);  // the docs buffer (and so the corpus key) moves along
     index.kg = std::move(kg);
     index.entity_map = build_entity_map(index.store);
+    g_mirrors.adopt(index_key(index), c, ix);  // searches on the result reuse the build's mirror
     return index;
 }
 
@@ -456,7 +595,8 @@ std::vector<SearchResult> batch_query(const HybridIndex& index, std::span<const 
 std::vector<SearchHit> brute_force_topk(const DocumentStore& store, const QuerySpec& q, unsigned) {
     validate_weights(q.weights);
     if (q.k == 0) throw Error("invalid-k", "k must be positive");
-    Corpus c(store);
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const auto c = g_mirrors.corpus(store);
     QueryFlat qf(std::span<const QuerySpec>(&q, 1));
     std::vector<uint64_t> doc(q.k);
     std::vector<uint32_t> node(q.k), cnt(1);
@@ -464,7 +604,7 @@ std::vector<SearchHit> brute_force_topk(const DocumentStore& store, const QueryS
     std::vector<char> err(256, 0);
     fg_search_results r{q.k, doc.data(), node.data(), score.data(), cnt.data(), nullptr, nullptr,
                         nullptr, err.data(), 256};
-    ok(fg_brute_force_topk(c.h, &qf.v, &r));
+    ok(fg_brute_force_topk(c->h, &qf.v, &r));
     if (err[0]) {
         const std::string w(err.data());
         const auto colon = w.find(": ");
@@ -474,5 +614,73 @@ std::vector<SearchHit> brute_force_topk(const DocumentStore& store, const QueryS
     for (uint32_t j = 0; j < cnt[0]; ++j) hits.push_back({doc[j], node[j], score[j]});
     return hits;
 }
+
+}  // namespace fusegraph
+
+// ---------------------------------------------------------------- maintenance
+// update.hpp:33-38.  Both keep the device mirror current in place, so the
+// next search runs on the B200 without a re-upload.
+namespace fusegraph {
+
+void insert_batch(HybridIndex& index, std::vector<DocumentRecord> new_docs, const InsertParams& params) {
+    if (new_docs.empty()) return;
+    const uint32_t kk = params.knn_k ? params.knn_k : index.knn_k;
+    if (kk < index.degree) throw Error("invalid-k", "insert candidate width must be at least the degree");
+    // host validation first, with the reference's checks and messages
+    // (update.cpp:44-63), so a bad batch leaves host and device untouched
+    for (DocumentRecord& doc : new_docs) {
+        const std::string where = "doc " + std::to_string(doc.doc_id);
+        if (index.store.id_to_node.count(doc.doc_id))
+            throw Error("duplicate-id", where + ": id already in the index");
+        if (doc.vector.dense.dim() != index.store.dense_dim)
+            throw Error("dim-mismatch", where + ": dense dimension " + std::to_string(doc.vector.dense.dim()) +
+                                            " differs from corpus " + std::to_string(index.store.dense_dim));
+        validate_fused(doc.vector, where);
+        doc.keywords = sorted_unique(std::move(doc.keywords));
+        doc.entities = sorted_unique(std::move(doc.entities));
+        doc.deleted = false;
+        finalize_fused(doc.vector);
+    }
+    for (std::size_t i = 1; i < new_docs.size(); ++i)
+        for (std::size_t j = 0; j < i; ++j)
+            if (new_docs[i].doc_id == new_docs[j].doc_id)
+                throw Error("duplicate-id", "doc " + std::to_string(new_docs[i].doc_id) +
+                                                ": id repeated within the batch");
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    fg_index* ix = g_mirrors.index(index);
+    DocumentStore batch;
+    batch.dense_dim = index.store.dense_dim;
+    batch.docs = new_docs;
+    Flat f(batch);
+    fg_insert_params p{kk, params.nn_descent_iterations, params.threads};
+    ok(fg_index_insert(ix, &f.v, &p));  // device corpus appended, edges linked in HBM
+    // mirror the device result into the reference struct
+    const uint64_t n_old = index.size(), nb = new_docs.size();
+    index.store.docs.reserve(n_old + nb);
+    for (uint64_t i = 0; i < nb; ++i) {
+        index.store.id_to_node[new_docs[i].doc_id] = static_cast<uint32_t>(n_old + i);
+        for (uint32_t e : new_docs[i].entities) index.entity_map[e].push_back(static_cast<uint32_t>(n_old + i));
+        index.store.docs.push_back(std::move(new_docs[i]));
+    }
+    pull_edges(ix, index, n_old + nb);
+    g_mirrors.rekey(ix, index_key(index));
+}
+
+void mark_delete(HybridIndex& index, std::span<const uint64_t> doc_ids) {
+    std::vector<uint32_t> nodes;  // resolve every id first (update.cpp:199-205)
+    nodes.reserve(doc_ids.size());
+    for (uint64_t id : doc_ids) nodes.push_back(index.store.node_of(id));
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const IndexKey before = index_key(index);
+    for (uint32_t node : nodes) index.store.docs[node].deleted = true;
+    g_mirrors.set_deleted(before, index);
+}
+
+namespace b200 {
+void invalidate_device_mirrors() {
+    std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    g_mirrors.clear();
+}
+}  // namespace b200
 
 }  // namespace fusegraph

@@ -1,9 +1,10 @@
 """Drop-in proof: the reference's OWN acceptance suite (tests/acceptance.cpp,
 unmodified, 9 criteria) linked against the reference library with
 integration/fusegraph_b200_shim.cpp in front, so index build, search,
-batch_query, NN-Descent, the refinery and brute-force truth run on the B200
-through libfgb200.so.  Built by `make -C integration` where /root/reference
-exists; the binary travels with the snapshot."""
+batch_query, insert_batch, mark_delete, NN-Descent, the refinery and
+brute-force truth run on the B200 through libfgb200.so.  Built by
+`make -C integration` where /root/reference exists; the binaries travel with
+the snapshot."""
 import os
 import subprocess
 
@@ -11,6 +12,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+MIRROR = os.path.join(ROOT, "oracle", "_ref", "mirror_check_b200")
 
 
 @pytest.mark.gpu
@@ -21,14 +23,21 @@ def test_reference_acceptance_suite_passes_on_b200():
     print(r.stdout)
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("[")]
     assert len(lines) == 9, r.stdout + r.stderr
+    # every criterion, including [6/9] (insert_batch forwarded to
+    # fg_index_insert: recall within 0.02 of a rebuild AND insert time under
+    # 40% of the rebuild's)
     for ln in lines:
-        if ln.startswith("[6/9]"):
-            # insert_batch is the reference's CPU code calling the shim's
-            # search once per new doc (one GPU launch each); the criterion's
-            # TIME bound (insert < 40% of a rebuild) compares that against a
-            # GPU rebuild.  Quality must still match: recall equal.
-            import re
-            m = re.search(r"recall@10 rebuild ([0-9.]+) vs insert ([0-9.]+)", ln)
-            assert m and float(m.group(2)) >= float(m.group(1)) - 0.02, ln
-        else:
-            assert "PASS" in ln, ln
+        assert "PASS" in ln, ln
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_device_mirror_lifetime():
+    """Cached device mirrors answer exactly like a fresh upload after
+    mark_delete, insert_batch and for indexes rebuilt in a reused slot."""
+    if not os.path.exists(MIRROR):
+        pytest.skip("integration binary not built (needs /root/reference at build time)")
+    r = subprocess.run([MIRROR], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("[PASS]") == 8, r.stdout
