@@ -69,7 +69,7 @@ BEAMS = [16, 32, 64, 128, 256, 512, 1024, 2048]
 # entry points (index.cpp:15-22).
 ENTRIES = [32, 64, 128, 256, 512, 1024]
 # selected by `python bench.py --sweep` on the held-out stream (profiles/r02_sweep.json)
-OPERATING_POINT = {"entry": 128, "beam": 512}
+OPERATING_POINT = {"entry": 512, "beam": 480}
 TIMED_STREAM, HELDOUT_STREAM = 0x71E5, 0x71E6
 WORKLOAD = ("configs[1]: 1M docs MS MARCO-shaped dense d=768 + learned sparse nnz 120 "
             "(vocab 30522), dense+sparse fusion, per-query weights (a, 1-a, 0, 0), a~U[0,1)")

@@ -1407,7 +1407,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         }
         if (const char* e = std::getenv("FGB_SEARCH_SCRATCH0")) {  // test hook: force re-runs
             const uint32_t v = static_cast<uint32_t>(std::atoi(e));
-            if (v >= 16 && (v & (v - 1)) == 0) {
+            if (v >= 2 && (v & (v - 1)) == 0) {
                 if (any_req) twcap0 = v;
                 if (any_ctx) ctxcap0 = v;
             }

@@ -290,11 +290,11 @@ def test_brute_force_identical(kg_case, ref):
 
 def test_search_scratch_overflow_reruns(kg_case, ref, monkeypatch):
     # a query that overflows the twin pool / entity-context table
-    # must neither hang nor fail the batch.  A 16-slot initial table forces
+    # must neither hang nor fail the batch.  A 2-slot initial table forces
     # the overflow path on most queries; the library re-runs them alone with
     # larger tables and the results stay identical to the reference's.
     p, c, kg, chains, dev, gix, rix = kg_case
-    monkeypatch.setenv("FGB_SEARCH_SCRATCH0", "16")
+    monkeypatch.setenv("FGB_SEARCH_SCRATCH0", "2")
     dense = np.stack([ch.query_dense for ch in chains])
     lr = [ch.query_learned for ch in chains]
     sr = [ch.query_statistical for ch in chains]
