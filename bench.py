@@ -498,7 +498,7 @@ def build_baseline():
     p = A.synth_params(**C1)
     c, kg, _ = synth.generate_corpus(p, 0)
     gpu_s = []
-    for _ in range(2):  # first run pays module load / allocations
+    for _ in range(3):  # the first run pays module load / allocations; min of the rest
         torch.cuda.synchronize()
         t0 = time.time()
         dc = fg.DeviceCorpus(c)
@@ -517,9 +517,9 @@ def build_baseline():
                 and np.array_equal(g["keyword"].idx, r["keyword"].idx)
                 and np.array_equal(g["norm_order"], r["norm_order"]))
     return {"workload": "configs[0]: 10K docs, d=128, learned+statistical nnz 64, degree 32, knn_k 64",
-            "gpu_seconds": round(gpu_s[-1], 3), "gpu_seconds_first": round(gpu_s[0], 3),
+            "gpu_seconds": round(min(gpu_s[1:]), 3), "gpu_seconds_runs": [round(x, 3) for x in gpu_s],
             "cpu_seconds": round(cpu_s, 2), "cores": cores, "cpu_model": cpu_model(),
-            "kind": "reference", "speedup": round(cpu_s / gpu_s[-1], 1), "identical_index": same}
+            "kind": "reference", "speedup": round(cpu_s / min(gpu_s[1:]), 1), "identical_index": same}
 
 
 def make_fixture(args):

@@ -382,6 +382,15 @@ int fg_brute_force_topk(const fg_corpus* c, const fg_query_view* q, fg_search_re
  * and the number of kernel launches it issued. */
 int fg_last_search_stats(const fg_index* ix, double* kernel_ms, uint64_t* launches);
 
+/* Diagnostics of the refinery's tensor-core candidate Gram (refine.cu,
+ * gram_tc_*; replaces the dense half of candidate_pair_scores,
+ * refine.cpp:11-23, with a certified split-bf16 tcgen05 product): pairs
+ * scored, pairs re-scored exactly because they fell within the error bound of
+ * a decision threshold, and (FGB_REFINE_TC_CHECK=1) the largest measured
+ * |approx - exact| / (|x||y|).  Counting is on while FGB_REFINE_TC_STATS=1
+ * or FGB_REFINE_TC_CHECK=1; reset != 0 zeroes the counters after reading. */
+int fg_refine_tc_stats(uint64_t* pairs, uint64_t* resolved, double* max_rel_err, int reset);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -17,10 +17,14 @@
 // the keyword lists drop ids that ended up semantic (refine.cpp:203-215).
 #include <cub/cub.cuh>
 
+#include <cuda_bf16.h>
+
 #include <algorithm>
+#include <cstdlib>
 
 #include "fg_cuda.hpp"
 #include "knn.cuh"
+#include "tcgen05.cuh"
 
 namespace fgb {
 namespace {
@@ -120,6 +124,13 @@ struct RefineArgs {
     uint32_t ukw_cap;      // max keyword list length
     uint64_t lo;           // first node of this launch (vertex-range sharding)
     uint64_t row0;         // node of row 0 of the list/output arrays (inserts: n_old)
+    // tensor-core Gram (gram_tc): on/off, bytes of the operand-stage / P
+    // union, the certification bound and optional counters
+    int tc;
+    uint32_t tc_union;
+    double tc_eps;
+    int tc_check;
+    unsigned long long* tc_stats;  // [0] pairs, [1] exact resolutions, [2] max |err|/(|a||b|) bits
 };
 
 // Generic (odd k) Gram: each thread owns up to kMaxPairsPerThread pairs.
@@ -275,16 +286,226 @@ __device__ __forceinline__ void gram_blocked(const RefineArgs& a, uint32_t k, co
     }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core Gram (tcgen05, kind::f16).  The dense part of every candidate
+// pair score is computed on the 5th-generation tensor cores as a split-bf16
+// product: each fp32 element a = hi + lo (+ r, |r| <= 2^-17 |a|) with
+// hi = bf16(a), lo = bf16(a - hi), and
+//     dense(x, y) ~= hi_x.hi_y + hi_x.lo_y + lo_x.hi_y
+// accumulated in fp32 in TMEM (3 MMAs per 16-wide K step).  The candidates'
+// rows are converted while staged (K-chunks of 64, double-buffered, 128-byte
+// swizzle), one thread issues M=64 (k <= 64) or M=128 MMAs, N = k rounded to
+// 16, and the accumulator is read back with tcgen05.ld.
+//
+// Certification.  |approx - dense_dot| <= eps * |x| |y| with eps = 2^-10
+// (kTcEps): the split drops <= 2^-15.5 |a_i b_i| per product, and 3*K/16 MMA
+// accumulations of 17 fp32 terms each lose <= 17 ulps of the running
+// magnitude (<= sum|a_i b_i| <= |x||y|) even with truncating alignment:
+// 144 * 17 * 2^-23 = 2.9e-4 at d = 768, 3.4x below eps (measured: see
+// FGB_REFINE_TC_CHECK and tests/test_gpu_refine_tc.py).  Every pair score
+// enters the refinery only through comparisons with four thresholds known up
+// front — csc[x], csc[y] (detours, strict <, refine.cpp:35) and sqnorm(x),
+// sqnorm(y) (IP prune, >=, refine.cpp:85) — so a pair whose approximate score
+// lies within eps of any of them is recomputed with the reference's exact
+// sequential fp64 chain (dense_dot, scoring.cpp:10-18) and all others decide
+// identically.  The sparse parts are exact merges either way.
+constexpr double kTcEps = 0.0009765625;  // 2^-10
+constexpr uint32_t kTcMaxItems = 4;      // (M rows x 8 chunks) / 256 threads, M <= 128
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void split8(const float4& x0, const float4& x1, uint4& hi, uint4& lo) {
+    const float f[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    float h[8], l[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        h[i] = __bfloat162float(__float2bfloat16_rn(f[i]));
+        l[i] = f[i] - h[i];  // exact in fp32
+    }
+    hi = make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
+                    pack_bf16x2(h[6], h[7]));
+    lo = make_uint4(pack_bf16x2(l[0], l[1]), pack_bf16x2(l[2], l[3]), pack_bf16x2(l[4], l[5]),
+                    pack_bf16x2(l[6], l[7]));
+}
+
+// exact dense_dot (scoring.cpp:10-18): one sequential fp64 chain
+__device__ double dense_exact(const DevCorpus& c, uint64_t x, uint64_t y) {
+    const float4* A = reinterpret_cast<const float4*>(c.dense + x * c.dstride);
+    const float4* B = reinterpret_cast<const float4*>(c.dense + y * c.dstride);
+    double acc = 0.0;
+    for (uint32_t t = 0; t < (c.dstride >> 2); ++t) {
+        const float4 p = __ldg(A + t), q = __ldg(B + t);
+        acc = __fma_rn((double)p.x, (double)q.x, acc);
+        acc = __fma_rn((double)p.y, (double)q.y, acc);
+        acc = __fma_rn((double)p.z, (double)q.z, acc);
+        acc = __fma_rn((double)p.w, (double)q.w, acc);
+    }
+    return acc;
+}
+
+// Dense approximation of every candidate pair into P[i*k + j] (i != j); the
+// operand stages alias P (they are dead before the epilogue writes it).
+__device__ void gram_tc_dense(const RefineArgs& a, uint32_t k, const uint32_t* cid, double* P,
+                              unsigned char* U, uint64_t* bar, uint32_t* tmem_slot) {
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t M = k <= 64 ? 64 : 128;
+    const uint32_t N = (k + 15) & ~15u;
+    const uint32_t ncols = N <= 32 ? 32 : N <= 64 ? 64 : 128;
+    const uint32_t tile = M * 128;  // bytes of one operand tile (M rows x 64 bf16)
+    const uint32_t nk = (a.c.dstride + 63) >> 6;
+    const uint32_t items = M * 8 / kRefineThreads;
+    const uint32_t idesc = idesc_bf16_f32(M, N);
+    if (warp == 0) {
+        tmem_alloc(tmem_slot, ncols);
+        tmem_relinquish();
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_proxy_async();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    float4 buf[kTcMaxItems][2];
+    auto load = [&](uint32_t kc) {
+#pragma unroll
+        for (uint32_t it = 0; it < kTcMaxItems; ++it) {
+            if (it >= items) break;
+            const uint32_t q = tid + it * kRefineThreads, r = q >> 3, c = q & 7;
+            const uint32_t col = kc * 64 + c * 8;
+            float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+            if (r < k && col < a.c.dstride) {
+                const float4* src = reinterpret_cast<const float4*>(a.c.dense + (uint64_t)cid[r] * a.c.dstride + col);
+                v0 = __ldg(src);
+                if (col + 4 < a.c.dstride) v1 = __ldg(src + 1);
+            }
+            buf[it][0] = v0;
+            buf[it][1] = v1;
+        }
+    };
+    auto store = [&](uint32_t st) {
+        unsigned char* hi_t = U + st * 2 * tile;
+        unsigned char* lo_t = hi_t + tile;
+#pragma unroll
+        for (uint32_t it = 0; it < kTcMaxItems; ++it) {
+            if (it >= items) break;
+            const uint32_t q = tid + it * kRefineThreads, r = q >> 3, c = q & 7;
+            const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4);
+            uint4 h, l;
+            split8(buf[it][0], buf[it][1], h, l);
+            *reinterpret_cast<uint4*>(hi_t + off) = h;
+            *reinterpret_cast<uint4*>(lo_t + off) = l;
+        }
+    };
+    load(0);
+    for (uint32_t kc = 0; kc < nk; ++kc) {
+        const uint32_t st = kc & 1;
+        if (kc >= 2) mbar_wait(&bar[st], ((kc - 2) >> 1) & 1);  // MMAs of chunk kc-2 done with stage st
+        store(st);
+        if (kc + 1 < nk) load(kc + 1);  // next chunk's loads in flight across the MMA issue
+        fence_proxy_async();            // generic-proxy smem writes -> tensor-core (async proxy) reads
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const unsigned char* hi_t = U + st * 2 * tile;
+            const unsigned char* lo_t = hi_t + tile;
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+                const uint64_t dh = sw128_desc(hi_t + 32 * j), dl = sw128_desc(lo_t + 32 * j);
+                mma_bf16_ss(tbase, dh, dh, idesc, (kc | j) ? 1u : 0u);
+                mma_bf16_ss(tbase, dh, dl, idesc, 1u);
+                mma_bf16_ss(tbase, dl, dh, idesc, 1u);
+            }
+            mma_commit(&bar[st]);
+        }
+    }
+    mbar_wait(&bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);  // completion is in issue order
+    tc_fence_after();
+    if (warp < 4) {
+        // M=128: row i in TMEM lane i; M=64: rows 16w..16w+15 in lanes 32w..32w+15
+        const uint32_t i = M == 128 ? 32 * warp + lane : 16 * warp + lane;
+        const bool valid = (M == 128 || lane < 16) && i < k;
+        for (uint32_t cb = 0; cb < N; cb += 16) {
+            float v[16];
+            tmem_ld16(tbase + ((32 * warp) << 16) + cb, v);
+            if (valid) {
+#pragma unroll
+                for (uint32_t c = 0; c < 16; ++c) {
+                    const uint32_t j = cb + c;
+                    if (j < k && j > i) {
+                        P[i * k + j] = (double)v[c];
+                        P[j * k + i] = (double)v[c];
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, ncols);
+    for (uint32_t j = tid; j < k; j += kRefineThreads) P[j * k + j] = 0.0;
+}
+
+// Sparse parts (exact merges) + certification of every pair (see above).
+__device__ void gram_tc_finish(const RefineArgs& a, uint32_t k, const uint32_t* cid, const double* csc, double* P) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    const uint32_t npairs = k * (k - 1) / 2;
+    unsigned long long nres = 0;
+    double maxrel = 0.0;
+#pragma unroll 1
+    for (uint32_t p = tid; p < npairs; p += nt) {
+        uint32_t i, j;
+        pair_of(p, k, i, j);
+        const uint64_t x = cid[i], y = cid[j];
+        const double d = P[i * k + j];
+        const double l = merge_dot(a.c.l_idx, a.c.l_val, a.c.l_off[x], a.c.l_nnz[x], a.c.l_off[y], a.c.l_nnz[y]);
+        const double t = merge_dot(a.c.s_idx, a.c.s_val, a.c.s_off[x], a.c.s_nnz[x], a.c.s_off[y], a.c.s_nnz[y]);
+        double s = __dadd_rn(__dadd_rn(d, l), t);
+        const double e = a.tc_eps * a.c.dnorm[x] * a.c.dnorm[y] * (1.0 + 1e-9) +
+                         1e-13 * (fabs(d) + fabs(l) + fabs(t));
+        const bool unc = fabs(s - csc[i]) <= e || fabs(s - csc[j]) <= e || fabs(s - a.c.sqnorm[x]) <= e ||
+                         fabs(s - a.c.sqnorm[y]) <= e;
+        if (unc || a.tc_check) {
+            const double dx = dense_exact(a.c, x, y);
+            if (a.tc_check) {
+                const double nn = a.c.dnorm[x] * a.c.dnorm[y];
+                if (nn > 0) maxrel = fmax(maxrel, fabs(d - dx) / nn);
+            }
+            s = __dadd_rn(__dadd_rn(dx, l), t);
+            nres += unc;
+        }
+        P[i * k + j] = s;
+        P[j * k + i] = s;
+    }
+    if (a.tc_stats) {
+        const unsigned long long np = (tid < npairs) ? (npairs - tid + nt - 1) / nt : 0;
+        atomicAdd(&a.tc_stats[0], np);
+        if (nres) atomicAdd(&a.tc_stats[1], nres);
+        if (maxrel > 0) atomicMax(&a.tc_stats[2], (unsigned long long)__double_as_longlong(maxrel));
+    }
+}
+
 __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t tc_bar[2];
+    __shared__ uint32_t tc_tmem;
     const uint32_t k = a.k;
     const uint64_t u = a.lo + blockIdx.x;
     const uint64_t ur = u - a.row0;  // row of u in the list / output arrays
     const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    // tensor-core path: P and the swizzled operand stages share a 1024-B aligned union
+    unsigned char* smem = smem_raw;
+    if (a.tc) smem += (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
     double* P = reinterpret_cast<double*>(smem);             // k*k
-    double* csc = P + k * k;                                 // k
-    float* tile = reinterpret_cast<float*>(csc + k);         // k * kTileStride
-    uint32_t* cid = reinterpret_cast<uint32_t*>(tile + tile_floats(k));
+    double* csc = reinterpret_cast<double*>(smem + (a.tc ? a.tc_union : k * k * 8));  // k
+    float* tile = reinterpret_cast<float*>(csc + k);         // k * kTileStride (SIMT Gram only)
+    uint32_t* cid = reinterpret_cast<uint32_t*>(tile + (a.tc ? 0 : tile_floats(k)));
     uint32_t* det = cid + k;
     uint32_t* order = det + k;   // rank -> candidate index
     uint32_t* kp = order + k;    // kept ranked positions
@@ -296,7 +517,7 @@ __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs 
     for (uint32_t j = tid; j < k; j += nt) {
         cid[j] = a.L_ids[ur * k + j];
         csc[j] = a.L_sc[ur * k + j];
-        P[j * k + j] = 0.0;
+        if (!a.tc) P[j * k + j] = 0.0;
     }
     for (uint32_t j = tid; j < a.kwcap; j += nt) kwset[j] = kEmpty;
     const uint64_t ub = a.c.kw_ptr[u], ue = a.c.kw_ptr[u + 1];
@@ -305,7 +526,11 @@ __global__ void __launch_bounds__(kRefineThreads) refine_node_kernel(RefineArgs 
     __syncthreads();
 
     // ---- candidate Gram (refine.cpp:11-23)
-    if ((k & 1) == 0) {
+    if (a.tc) {
+        gram_tc_dense(a, k, cid, P, smem, tc_bar, &tc_tmem);
+        __syncthreads();
+        gram_tc_finish(a, k, cid, csc, P);
+    } else if ((k & 1) == 0) {
         gram_blocked(a, k, cid, P, reinterpret_cast<double*>(tile));
     } else {
         gram_pairs(a, k, cid, P, tile);
@@ -523,6 +748,25 @@ __global__ void merge_reverse_kernel(uint64_t n, uint32_t k, uint32_t degree, co
 
 }  // namespace
 
+// Diagnostics of the tensor-core Gram (FGB_REFINE_TC_STATS=1 or
+// FGB_REFINE_TC_CHECK=1): counters on the current device, read through
+// fg_refine_tc_stats.
+unsigned long long* g_tc_stats = nullptr;
+int g_tc_stats_dev = -1;
+unsigned long long* refine_tc_stats_ptr() {
+    const char* se = std::getenv("FGB_REFINE_TC_STATS");
+    const char* ce = std::getenv("FGB_REFINE_TC_CHECK");
+    if (!((se && se[0] == '1') || (ce && ce[0] == '1'))) return nullptr;
+    int dev = 0;
+    FGB_CUDA(cudaGetDevice(&dev));
+    if (!g_tc_stats || g_tc_stats_dev != dev) {
+        FGB_CUDA(cudaMalloc(&g_tc_stats, 4 * sizeof(unsigned long long)));
+        FGB_CUDA(cudaMemset(g_tc_stats, 0, 4 * sizeof(unsigned long long)));
+        g_tc_stats_dev = dev;
+    }
+    return g_tc_stats;
+}
+
 void refine_alloc(const DevKnn& g, uint32_t degree, RefineOut& out, cudaStream_t s) {
     const uint64_t n = g.n;
     const uint32_t k = g.k;
@@ -555,8 +799,20 @@ void refine_nodes(const fg_corpus& c, const DevKnn& g, bool per_neighbour, uint6
     RefineArgs a{c.dc, k, degree, per_neighbour ? 1 : 0, g.ids.get(), g.scores.get(),
                  out.ordered.get(), out.ordered_sc.get(), out.detours.get(), out.kept.get(),
                  out.kept_count.get(), out.keyword.get(), out.kw_count.get(), kwcap, max_kw, lo, row0};
-    const size_t sm = static_cast<size_t>(k) * k * 8 + k * 8 + static_cast<size_t>(tile_floats(k)) * 4 +
-                      5 * k * 4 + static_cast<size_t>(kwcap) * 4 + static_cast<size_t>(max_kw) * 4 + 16;
+    // dense Gram on the tensor cores (gram_tc_dense) for k <= 128;
+    // FGB_REFINE_TC=0 keeps the exact fp64 SIMT Gram (A/B and fallback tests)
+    const char* te = std::getenv("FGB_REFINE_TC");
+    a.tc = (!te || te[0] != '0') && k <= 128 && c.dc.dnorm != nullptr;
+    const uint32_t tc_m = k <= 64 ? 64 : 128;
+    a.tc_union = static_cast<uint32_t>(std::max<size_t>(static_cast<size_t>(k) * k * 8, 4ull * tc_m * 128));
+    a.tc_eps = kTcEps;
+    if (const char* e = std::getenv("FGB_REFINE_TC_EPS_SCALE")) a.tc_eps *= std::max(1.0, std::atof(e));
+    const char* ce = std::getenv("FGB_REFINE_TC_CHECK");
+    a.tc_check = ce && ce[0] == '1';
+    a.tc_stats = refine_tc_stats_ptr();
+    const size_t body = a.tc ? 1024 + a.tc_union + k * 8 : static_cast<size_t>(k) * k * 8 + k * 8 +
+                                                            static_cast<size_t>(tile_floats(k)) * 4;
+    const size_t sm = body + 5 * k * 4 + static_cast<size_t>(kwcap) * 4 + static_cast<size_t>(max_kw) * 4 + 16;
     if (sm > 227 * 1024)
         throw Error("invalid-k", "refinery shared memory exceeds the SM (" + std::to_string(sm) + " B)");
     FGB_CUDA(cudaFuncSetAttribute(refine_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -654,3 +910,21 @@ int fg_refine(const fg_corpus* c, const fg_knn_lists* knn, const fg_refine_param
 }
 
 }  // extern "C"
+
+extern "C" int fg_refine_tc_stats(uint64_t* pairs, uint64_t* resolved, double* max_rel_err, int reset) {
+    return fgb::guarded([&] {
+        unsigned long long h[4] = {0, 0, 0, 0};
+        if (fgb::g_tc_stats) {
+            FGB_CUDA(cudaDeviceSynchronize());
+            FGB_CUDA(cudaMemcpy(h, fgb::g_tc_stats, sizeof(h), cudaMemcpyDeviceToHost));
+            if (reset) FGB_CUDA(cudaMemset(fgb::g_tc_stats, 0, sizeof(h)));
+        }
+        if (pairs) *pairs = h[0];
+        if (resolved) *resolved = h[1];
+        if (max_rel_err) {
+            double d;
+            std::memcpy(&d, &h[2], 8);
+            *max_rel_err = d;
+        }
+    });
+}

@@ -326,3 +326,10 @@ def recall_at_k(result, truth, k: int) -> float:
     t = set(int(x) for x in truth)
     hits = sum(1 for x in list(result)[:k] if int(x) in t)
     return hits / k
+
+
+def refine_tc_stats(reset: bool = True) -> dict:
+    """Counters of the refinery's tensor-core Gram (fg_refine_tc_stats)."""
+    pairs, res, mx = C.c_uint64(), C.c_uint64(), C.c_double()
+    check(lib().fg_refine_tc_stats(C.byref(pairs), C.byref(res), C.byref(mx), int(reset)))
+    return {"pairs": pairs.value, "resolved": res.value, "max_rel_err": mx.value}
