@@ -24,10 +24,14 @@
 // Errors come back as fusegraph::Error with the reference's codes.
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "fg_b200.h"
@@ -557,15 +561,29 @@ HybridIndex build_hybrid_index(DocumentStore store, KnowledgeGraph kg, const Bui
         return index;
     }
     std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const bool timing = [] {
+        const char* te = std::getenv("FGB_HOST_TIMING");
+        return te && te[0] != '0';
+    }();
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!timing) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[shim build] %-20s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
     const auto c = g_mirrors.corpus(store);
+    mark("corpus mirror");
     KgFlat kf(kg);
     fg_build_params bp{params.degree, params.knn_k, params.knn_iterations, params.seed,
                        params.logical_cap, params.default_entity_hops,
                        params.per_neighbour_keyword_check ? 1 : 0};
     fg_index* ix = nullptr;
     ok(fg_index_build(c->h, &kf.v, &bp, &ix));
+    mark("fg_index_build");
     try {
         pull_edges(ix, index, n);
+        mark("pull_edges");
     } catch (...) {
         fg_index_free(ix);
         throw;
@@ -573,7 +591,9 @@ HybridIndex build_hybrid_index(DocumentStore store, KnowledgeGraph kg, const Bui
     index.store = std::move(store);  // the docs buffer (and so the corpus key) moves along
     index.kg = std::move(kg);
     index.entity_map = build_entity_map(index.store);
+    mark("host index");
     g_mirrors.adopt(index_key(index), c, ix);  // searches on the result reuse the build's mirror
+    mark("adopt");
     return index;
 }
 
@@ -641,19 +661,36 @@ void insert_batch(HybridIndex& index, std::vector<DocumentRecord> new_docs, cons
         doc.deleted = false;
         finalize_fused(doc.vector);
     }
-    for (std::size_t i = 1; i < new_docs.size(); ++i)
-        for (std::size_t j = 0; j < i; ++j)
-            if (new_docs[i].doc_id == new_docs[j].doc_id)
-                throw Error("duplicate-id", "doc " + std::to_string(new_docs[i].doc_id) +
-                                                ": id repeated within the batch");
+    {  // update.cpp:58-62 reports the first doc whose id occurs earlier in the batch
+        std::unordered_set<uint64_t> seen;
+        seen.reserve(new_docs.size() * 2);
+        for (const DocumentRecord& doc : new_docs)
+            if (!seen.insert(doc.doc_id).second)
+                throw Error("duplicate-id", "doc " + std::to_string(doc.doc_id) + ": id repeated within the batch");
+    }
     std::lock_guard<std::mutex> lock(g_mirrors.mu);
+    const bool timing = [] {
+        const char* te = std::getenv("FGB_HOST_TIMING");
+        return te && te[0] != '0';
+    }();
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!timing) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[shim insert] %-20s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
+    mark("validate");
     fg_index* ix = g_mirrors.index(index);
+    mark("mirror lookup");
     DocumentStore batch;
     batch.dense_dim = index.store.dense_dim;
     batch.docs = new_docs;
     Flat f(batch);
     fg_insert_params p{kk, params.nn_descent_iterations, params.threads};
+    mark("flatten");
     ok(fg_index_insert(ix, &f.v, &p));  // device corpus appended, edges linked in HBM
+    mark("fg_index_insert");
     // mirror the device result into the reference struct
     const uint64_t n_old = index.size(), nb = new_docs.size();
     index.store.docs.reserve(n_old + nb);
@@ -662,8 +699,11 @@ void insert_batch(HybridIndex& index, std::vector<DocumentRecord> new_docs, cons
         for (uint32_t e : new_docs[i].entities) index.entity_map[e].push_back(static_cast<uint32_t>(n_old + i));
         index.store.docs.push_back(std::move(new_docs[i]));
     }
+    mark("host docs");
     pull_edges(ix, index, n_old + nb);
+    mark("pull_edges");
     g_mirrors.rekey(ix, index_key(index));
+    mark("rekey");
 }
 
 void mark_delete(HybridIndex& index, std::span<const uint64_t> doc_ids) {

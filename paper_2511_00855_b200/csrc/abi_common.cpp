@@ -19,6 +19,15 @@ void clear_last_error() {
     t_code.clear();
     t_what.clear();
 }
+
+void HostTimer::mark(const char* what) {
+    if (!on) return;
+    if (mode() == 1) cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[host timing] %-14s %-26s %8.3f ms\n", scope, what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+}
 }  // namespace fgb
 
 extern "C" {

@@ -186,52 +186,78 @@ __device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, ui
     for (int k = 0; k < NQ4; ++k) b[k] = __ldg(row + min(k * 32 + lane, n4 - 1));
 }
 
+// Rows in flight per round trip of dense_group: narrow rows (d <= 256) keep
+// more of them in registers, so a batch of F candidates costs F/kRows
+// dependent round trips instead of F/2.
+template <int NQ4>
+constexpr int dense_rows() { return NQ4 == 1 ? 8 : (NQ4 == 2 ? 4 : 2); }
+
+// Reduce-scatter of R per-lane partial sums (R a power of two <= 8): row r's
+// total (over all 32 lanes) ends in lanes [r * 32/R, (r + 1) * 32/R).
+template <int R>
+__device__ __forceinline__ double reduce_scatter(double (&x)[R], uint32_t lane) {
+#pragma unroll
+    for (int cnt = R, stride = 16; cnt > 1; cnt >>= 1, stride >>= 1) {
+        const bool b = (lane & stride) != 0;
+#pragma unroll
+        for (int i = 0; i < cnt / 2; ++i) {
+            const double send = b ? x[i] : x[i + cnt / 2];
+            x[i] = (b ? x[i + cnt / 2] : x[i]) + __shfl_xor_sync(kFull, send, stride);
+        }
+    }
+    double r = x[0];
+#pragma unroll
+    for (int stride = 16 / R; stride > 0; stride >>= 1) r += __shfl_xor_sync(kFull, r, stride);
+    return r;
+}
+
 // Warp-cooperative approximate dense dot (coalesced 512-B loads per warp
-// instruction) for every lane-held node in `mask`, two rows per round trip;
-// fp32 partials of 4 elements, accumulated in fp64.
+// instruction) for every lane-held node in `mask`, dense_rows<NQ4>() rows
+// per round trip; fp32 partials of 4 elements, accumulated in fp64.
 template <int NQ4>
 __device__ __forceinline__ double dense_group(const DevCorpus& c, const float* qd, uint32_t node, uint32_t lane,
                                               uint32_t mask) {
+    constexpr int R = dense_rows<NQ4>();
     double mine = 0.0;
     const float4* q4 = reinterpret_cast<const float4*>(qd);
     const uint32_t n4 = c.dstride >> 2;
     uint32_t m = mask;
 #pragma unroll 1
     while (m) {
+        uint32_t j[R];
         const uint32_t j0 = __ffs(m) - 1;
-        m &= m - 1;
-        const bool two = m != 0;
-        const uint32_t j1 = two ? __ffs(m) - 1 : j0;
-        if (two) m &= m - 1;
-        const uint32_t n0 = __shfl_sync(kFull, node, j0), n1 = __shfl_sync(kFull, node, j1);
-        float4 ra[NQ4], rb[NQ4];
-        dense_load<NQ4>(c, n0, lane, ra);
-        dense_load<NQ4>(c, n1, lane, rb);  // (j1 == j0 when alone: an L1 hit, result unused)
-        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {  // (missing rows repeat j0: L1 hits, results unused)
+            j[r] = m ? __ffs(m) - 1 : j0;
+            m &= m - 1;
+        }
+        float4 rows[R][NQ4];
+#pragma unroll
+        for (int r = 0; r < R; ++r) dense_load<NQ4>(c, __shfl_sync(kFull, node, j[r]), lane, rows[r]);
+        double s[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) s[r] = 0.0;
 #pragma unroll
         for (int k = 0; k < NQ4; ++k) {
             const uint32_t col = k * 32 + lane;
             if (col < n4) {
                 const float4 q = q4[col];
-                float pa = q.x * ra[k].x, pb = q.x * rb[k].x;
-                pa = __fmaf_rn(q.y, ra[k].y, pa);
-                pb = __fmaf_rn(q.y, rb[k].y, pb);
-                pa = __fmaf_rn(q.z, ra[k].z, pa);
-                pb = __fmaf_rn(q.z, rb[k].z, pb);
-                pa = __fmaf_rn(q.w, ra[k].w, pa);
-                pb = __fmaf_rn(q.w, rb[k].w, pb);
-                sa += (double)pa;
-                sb += (double)pb;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float p = q.x * rows[r][k].x;
+                    p = __fmaf_rn(q.y, rows[r][k].y, p);
+                    p = __fmaf_rn(q.z, rows[r][k].z, p);
+                    p = __fmaf_rn(q.w, rows[r][k].w, p);
+                    s[r] += (double)p;
+                }
             }
         }
-        // reduce-scatter of the pair: lanes 0-15 end with a's sum, 16-31 with b's
-        const bool hi = lane >= 16;
-        double r = (hi ? sb : sa) + __shfl_xor_sync(kFull, hi ? sa : sb, 16);
+        const double tot = reduce_scatter<R>(s, lane);
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
-        const double ga = __shfl_sync(kFull, r, 0), gb = __shfl_sync(kFull, r, 16);
-        if (lane == j0) mine = ga;
-        if (two && lane == j1) mine = gb;
+        for (int r = 0; r < R; ++r) {
+            const double g = __shfl_sync(kFull, tot, r * (32 / R));
+            if (lane == j[r] && (r == 0 || j[r] != j0)) mine = g;
+        }
     }
     return mine;
 }

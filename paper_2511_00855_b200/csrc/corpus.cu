@@ -325,6 +325,41 @@ void corpus_append(fg_corpus& c, const fg_corpus_view& v) {
     corpus_finalize(c);
 }
 
+CorpusMark corpus_mark(const fg_corpus& c) { return {c.n, c.l_nnz_total4, c.s_nnz_total4}; }
+
+void corpus_rollback(fg_corpus& c, const CorpusMark& m) {
+    // the device arrays keep their (unused) tail; maxima and vocabulary
+    // bounds stay as upper bounds (they only widen error bounds / smem sizing)
+    c.n = m.n;
+    c.dc.n = m.n;
+    c.l_nnz_total4 = m.l4;
+    c.s_nnz_total4 = m.s4;
+    c.doc_id.resize(m.n);
+    c.deleted_h.resize(m.n);
+    c.sqnorm_h.resize(m.n);
+    for (HostList* h : {&c.keywords, &c.entities}) {
+        h->ptr.resize(m.n + 1);
+        h->idx.resize(h->ptr.back());
+    }
+}
+
+DevCorpus corpus_rows(const DevCorpus& d, uint64_t first, uint64_t count) {
+    DevCorpus v = d;
+    v.n = count;
+    v.dense = d.dense + first * d.dstride;
+    v.l_off = d.l_off + first;
+    v.l_nnz = d.l_nnz + first;
+    v.s_off = d.s_off + first;
+    v.s_nnz = d.s_nnz + first;
+    v.kw_ptr = d.kw_ptr + first;
+    v.ent_ptr = d.ent_ptr + first;
+    v.sqnorm = d.sqnorm + first;
+    v.dnorm = d.dnorm + first;
+    v.deleted = d.deleted + first;
+    v.meta = d.meta ? d.meta + first : nullptr;
+    return v;  // idx/val arrays stay shared: offsets are absolute
+}
+
 }  // namespace fgb
 
 using namespace fgb;
@@ -337,6 +372,7 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
         if (v->n == 0) throw Error("empty-corpus", "corpus holds no documents");
         if (v->n >= 0x7FFFFFFFull) throw Error("invalid-argument", "corpus exceeds 2^31-1 nodes");
         require_device(device);
+        HostTimer ht("corpus_upload");
         auto c = std::make_unique<fg_corpus>();
         c->device = device;
         c->n = v->n;
@@ -407,6 +443,7 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             for (uint64_t i = 0; i < n; ++i) c->deleted_h[i] = v->deleted[i] ? 1 : 0;
         c->deleted.upload(c->deleted_h, s);
         corpus_finalize(*c);
+        ht.mark("done");
         *out = c.release();
     });
 }

@@ -6,6 +6,7 @@
 
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,15 @@ inline void require_device(int device) {
     FGB_CUDA(cudaSetDevice(device));
 }
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// on a private stream, release threshold unlimited): freed blocks stay cached,
+// so repeated API calls (batch_query, insert_batch, small builds) run without
+// driver allocations.  A free first synchronises the device — the same
+// guarantee cudaFree gives — so no queued kernel can still use the block when
+// the pool hands it out again.  (abi_common.cpp)
+void* pool_alloc(size_t bytes, int* device);
+void pool_free(void* p, int device) noexcept;
+
 // Owning device allocation.
 template <typename T>
 class DevBuf {
@@ -44,7 +54,7 @@ public:
     explicit DevBuf(size_t n) { alloc(n); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), dev_(o.dev_) {
         o.p_ = nullptr;
         o.n_ = 0;
     }
@@ -53,6 +63,7 @@ public:
             release();
             p_ = o.p_;
             n_ = o.n_;
+            dev_ = o.dev_;
             o.p_ = nullptr;
             o.n_ = 0;
         }
@@ -62,14 +73,14 @@ public:
 
     void alloc(size_t n) {
         release();
+        if (n) p_ = static_cast<T*>(pool_alloc(n * sizeof(T), &dev_));
         n_ = n;
-        if (n) FGB_CUDA(cudaMalloc(&p_, n * sizeof(T)));
     }
     void ensure(size_t n) {
         if (n > n_) alloc(n);
     }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) pool_free(p_, dev_);
         p_ = nullptr;
         n_ = 0;
     }
@@ -90,6 +101,7 @@ public:
 private:
     T* p_ = nullptr;
     size_t n_ = 0;
+    int dev_ = 0;
 };
 
 // Grow-only page-locked host buffer (device->host staging at DMA speed).
@@ -206,11 +218,32 @@ struct SearchIo {
     PinnedBuf<unsigned char> host;
 };
 
+// Search scratch of one device, shared by all its indexes: per-warp visited /
+// expanded / twin bitsets (all-zero between calls: every kernel clears what
+// it set), touched lists, twin pools and entity-context tables, plus the
+// batch I/O above.  One batch_query at a time per device holds `mu`; every
+// call synchronises its stream before releasing it.
+struct SearchWorkspace {
+    std::mutex mu;
+    SearchIo io;
+    DevBuf<uint32_t> bits;
+    DevBuf<uint32_t> lists;
+    DevBuf<unsigned char> misc;
+};
+
 inline uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
 
 // Derived device state of an uploaded corpus (norms, gather records, maxima).
 void corpus_finalize(fg_corpus& c);
 // Appends the rows of `v` (insert_batch); validation is the caller's.
 void corpus_append(fg_corpus& c, const fg_corpus_view& v);
+// Undo of corpus_append (insert_batch failing after the append).
+struct CorpusMark {
+    uint64_t n, l4, s4;
+};
+CorpusMark corpus_mark(const fg_corpus& c);
+void corpus_rollback(fg_corpus& c, const CorpusMark& m);
+// Zero-copy view of rows [first, first + count) as a corpus of `count` rows.
+DevCorpus corpus_rows(const DevCorpus& d, uint64_t first, uint64_t count);
 
 }  // namespace fgb

@@ -68,3 +68,29 @@ inline double uniform01_bits(uint64_t x) { return static_cast<double>(x >> 11) *
 inline double uniform01(SplitMix64& rng) { return uniform01_bits(rng.next()); }
 
 }  // namespace fgb
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
+namespace fgb {
+// Dev tool: FGB_HOST_TIMING=1 prints per-phase wall times of host entry
+// points (each mark synchronises the device first, so phases include their
+// GPU work); =2 prints the same marks without synchronising.  Off by
+// default: no syncs, no output.
+struct HostTimer {
+    const char* scope;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit HostTimer(const char* s) : scope(s), on(enabled()), t(std::chrono::steady_clock::now()) {}
+    static int mode() {
+        static const int e = [] {
+            const char* v = std::getenv("FGB_HOST_TIMING");
+            return v ? std::atoi(v) : 0;
+        }();
+        return e;
+    }
+    static bool enabled() { return mode() != 0; }
+    void mark(const char* what);
+};
+}  // namespace fgb

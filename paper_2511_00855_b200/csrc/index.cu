@@ -3,6 +3,8 @@
 // host: entity map and logical edges (logical.cpp:9-68), KG adjacency
 // (types.cpp:29-45) and the norm order (index.cpp:12-23).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <cmath>
 #include <unordered_set>
@@ -10,6 +12,7 @@
 #include <array>
 #include <chrono>
 #include <numeric>
+#include <exception>
 #include <thread>
 
 #include "index.hpp"
@@ -110,6 +113,18 @@ void logical_for(const fg_corpus& c, uint32_t node, const HostKg& kg,
 __global__ void gather_meta_kernel(const uint4* meta, const uint32_t* ids, uint64_t m, uint4* out) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i < m) out[i] = meta[ids[i]];
+}
+
+std::shared_ptr<SearchWorkspace> search_workspace(int device) {
+    static std::mutex mu;
+    static std::map<int, std::weak_ptr<SearchWorkspace>> live;
+    std::lock_guard<std::mutex> lock(mu);
+    std::shared_ptr<SearchWorkspace> w = live[device].lock();
+    if (!w) {
+        w = std::make_shared<SearchWorkspace>();
+        live[device] = w;
+    }
+    return w;
 }
 
 void index_finish(fg_index& ix, const fg_kg_view* kgv) {
@@ -259,6 +274,8 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
     const uint32_t kk = p.knn_k ? p.knn_k : ix.knn_k;
     if (batch == 0) return;
     if (kk < d) throw Error("invalid-k", "insert candidate width must be at least the degree");
+    HostTimer mark_t("insert");
+    auto mark = [&](const char* what) { mark_t.mark(what); };
 
     // ---- validate before touching anything (update.cpp:43-63)
     std::unordered_set<uint64_t> ids(c.doc_id.begin(), c.doc_id.end());
@@ -276,10 +293,13 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
         check_sparse(in.learned, i, where, "learned");
         check_sparse(in.statistical, i, where, "statistical");
     }
-    for (uint64_t i = 1; i < batch; ++i)
-        for (uint64_t j = 0; j < i; ++j)
-            if (doc_id[i] == doc_id[j])
+    {  // update.cpp:58-62 reports the first doc whose id occurs earlier in the batch
+        std::unordered_set<uint64_t> seen;
+        seen.reserve(batch * 2);
+        for (uint64_t i = 0; i < batch; ++i)
+            if (!seen.insert(doc_id[i]).second)
                 throw Error("duplicate-id", "doc " + std::to_string(doc_id[i]) + ": id repeated within the batch");
+    }
     // keywords / entities sorted unique (update.cpp:58-59), keywords default to
     // the statistical support (make_document, corpus.cpp:113-117)
     auto sorted_unique = [&](const fg_list_view& lv, bool kw) {
@@ -304,8 +324,73 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
     v.keywords = fg_list_view{kws.ptr.data(), kws.idx.data()};
     v.entities = fg_list_view{ents.ptr.data(), ents.idx.data()};
 
-    // ---- (a) nearest existing nodes through the current graph (update.cpp:18-29)
+    mark("validate");
+    // ---- append the documents first (update.cpp:94-103): the new rows have no
+    // edges yet, so (a) cannot reach them, and (b) reads them in place
+    const CorpusMark before = corpus_mark(c);
+    corpus_append(c, v);
+    struct Rollback {
+        fg_corpus& c;
+        CorpusMark m;
+        bool armed = true;
+        ~Rollback() {
+            if (armed) corpus_rollback(c, m);
+        }
+    } rollback{c, before};
+    mark("corpus append");
+
+    // ---- (b) neighbour-descent among the batch itself (update.cpp:71-88), on
+    // a zero-copy view of rows [n_old, n_old + batch) (local ids 0..batch-1, as
+    // the reference's batch store), on its own stream from a helper thread
+    // while (a) searches the current graph
     std::vector<std::vector<Cand>> from_index(batch), from_batch(batch);
+    std::exception_ptr b_err;
+    std::thread tb([&] {
+        try {
+            FGB_CUDA(cudaSetDevice(c.device));
+            if (batch > 1) {
+                fg_corpus view;  // non-owning: its DevBufs stay empty
+                view.device = c.device;
+                view.n = batch;
+                view.dim = c.dim;
+                view.dstride = c.dstride;
+                view.max_lnnz = c.max_lnnz;
+                view.max_snnz = c.max_snnz;
+                view.l_vocab = c.l_vocab;
+                view.s_vocab = c.s_vocab;
+                view.learned_dim = c.learned_dim;
+                view.statistical_dim = c.statistical_dim;
+                view.max_sqnorm = c.max_sqnorm;
+                view.max_dnorm = c.max_dnorm;
+                view.dc = corpus_rows(c.dc, n_old, batch);
+                FGB_CUDA(cudaStreamCreateWithFlags(&view.stream, cudaStreamNonBlocking));
+                struct StreamGuard {
+                    cudaStream_t s;
+                    ~StreamGuard() { cudaStreamDestroy(s); }
+                } sg{view.stream};
+                DevKnn g;
+                const uint32_t kb = std::min<uint32_t>(kk, static_cast<uint32_t>(batch - 1));
+                knn_build_device(view, kb, p.nn_descent_iterations, 0.01, mix_seed(ix.seed, n_old), g, view.stream);
+                std::vector<uint32_t> gid(batch * g.k);
+                std::vector<double> gsc(batch * g.k);
+                g.ids.download(gid.data(), gid.size(), view.stream);
+                g.scores.download(gsc.data(), gsc.size(), view.stream);
+                FGB_CUDA(cudaStreamSynchronize(view.stream));
+                for (uint64_t i = 0; i < batch; ++i)
+                    for (uint32_t j = 0; j < g.k; ++j)
+                        from_batch[i].push_back({static_cast<uint32_t>(n_old + gid[i * g.k + j]), gsc[i * g.k + j]});
+            }
+        } catch (...) {
+            b_err = std::current_exception();
+        }
+    });
+    struct Joiner {
+        std::thread& t;
+        ~Joiner() {
+            if (t.joinable()) t.join();
+        }
+    } joiner{tb};
+    // ---- (a) nearest existing nodes through the current graph (update.cpp:18-29)
     {
         std::vector<fg_weights> w(batch, fg_weights{1.f, 1.f, 1.f, 0.f});
         std::vector<uint32_t> kq(batch, kk), bq(batch, 2 * kk);
@@ -340,32 +425,16 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
             for (uint32_t j = 0; j < rc[i]; ++j) from_index[i].push_back({rn[i * kk + j], rs[i * kk + j]});
         }
     }
-    // ---- (b) neighbour-descent among the batch itself (update.cpp:71-88)
-    if (batch > 1) {
-        fg_corpus* tmp = nullptr;
-        if (fg_corpus_upload(&v, c.device, &tmp) != FG_OK) throw Error(fg_last_error_code(), fg_last_error_message());
-        std::unique_ptr<fg_corpus, int (*)(fg_corpus*)> tg(tmp, fg_corpus_free);
-        DevKnn g;
-        const uint32_t kb = std::min<uint32_t>(kk, static_cast<uint32_t>(batch - 1));
-        knn_build_device(*tmp, kb, p.nn_descent_iterations, 0.01, mix_seed(ix.seed, n_old), g, tmp->stream);
-        std::vector<uint32_t> gid(batch * g.k);
-        std::vector<double> gsc(batch * g.k);
-        g.ids.download(gid.data(), gid.size(), tmp->stream);
-        g.scores.download(gsc.data(), gsc.size(), tmp->stream);
-        FGB_CUDA(cudaStreamSynchronize(tmp->stream));
-        for (uint64_t i = 0; i < batch; ++i)
-            for (uint32_t j = 0; j < g.k; ++j)
-                from_batch[i].push_back({static_cast<uint32_t>(n_old + gid[i * g.k + j]), gsc[i * g.k + j]});
-    }
+    mark("search candidates");
+    tb.join();
+    if (b_err) std::rethrow_exception(b_err);
     for (uint64_t i = 0; i < batch; ++i)
         if (from_index[i].size() + from_batch[i].size() < d)
             throw Error("corpus-too-small", "doc " + std::to_string(doc_id[i]) + ": only " +
                                                 std::to_string(from_index[i].size() + from_batch[i].size()) +
                                                 " insert candidates for degree " + std::to_string(d));
-
-    // ---- append the documents (update.cpp:94-103)
-    corpus_append(c, v);
-
+    mark("batch nn-descent");
+    rollback.armed = false;  // past the last check: the insert commits
     // ---- merged candidates, the per-node refinery (update.cpp:105-125)
     std::vector<std::vector<Cand>> cands(batch);
     for (uint64_t i = 0; i < batch; ++i) {
@@ -413,6 +482,7 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
         i0 = i1;
     }
 
+    mark("refinery");
     // ---- reverse half among the batch, new semantic / keyword lists (update.cpp:127-165)
     const uint32_t half = d / 2;
     std::vector<std::vector<std::pair<uint32_t, uint32_t>>> keepers(batch);  // (pos, keeper)
@@ -446,44 +516,47 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
             if (!has(id)) new_kw[i].push_back(id);
     }
 
+    mark("new lists");
     // ---- existing nodes: weakest reverse slot replacement (update.cpp:167-193),
     // in the reference's order over exact pair scores computed on the GPU
+    // pair list: per touched w its (d - half) reverse-slot pairs once, then one
+    // (w, u) pair per kept edge; indices into `ps` replace hash lookups
     std::vector<uint32_t> pa, pb;
-    std::vector<char> touched(n_old, 0);
-    for (uint64_t i = 0; i < batch; ++i)
-        for (uint32_t w : kept[i]) {
+    std::vector<uint64_t> slot_base(n_old, ~0ull);
+    std::vector<std::vector<uint64_t>> edge_pair(batch);
+    for (uint64_t i = 0; i < batch; ++i) {
+        edge_pair[i].assign(kept[i].size(), ~0ull);
+        for (size_t q = 0; q < kept[i].size(); ++q) {
+            const uint32_t w = kept[i][q];
             if (w >= n_old) continue;
-            if (!touched[w]) {
-                touched[w] = 1;
+            if (slot_base[w] == ~0ull) {
+                slot_base[w] = pa.size();
                 for (uint32_t sl = half; sl < d; ++sl) {
                     pa.push_back(w);
                     pb.push_back(ix.semantic_h[static_cast<uint64_t>(w) * d + sl]);
                 }
             }
+            edge_pair[i][q] = pa.size();
             pa.push_back(w);
             pb.push_back(static_cast<uint32_t>(n_old + i));
         }
+    }
     std::vector<double> ps(pa.size());
     if (!pa.empty() &&
         fg_pair_scores(&c, pa.data(), pb.data(), pa.size(), ps.data()) != FG_OK)
         throw Error(fg_last_error_code(), fg_last_error_message());
-    std::unordered_map<uint64_t, double> pair_score;
-    for (size_t q = 0; q < pa.size(); ++q) pair_score[(static_cast<uint64_t>(pa[q]) << 32) | pb[q]] = ps[q];
-    std::unordered_map<uint32_t, std::vector<double>> slot_scores;
+    // current score of each reverse slot of w (slot_base[w] + sl - half),
+    // updated in place as slots are replaced (update.cpp:167-193)
     for (uint64_t i = 0; i < batch; ++i) {
         const uint32_t u = static_cast<uint32_t>(n_old + i);
-        for (uint32_t w : kept[i]) {
+        for (size_t q = 0; q < kept[i].size(); ++q) {
+            const uint32_t w = kept[i][q];
             if (w >= n_old) continue;
             uint32_t* sem = ix.semantic_h.data() + static_cast<uint64_t>(w) * d;
             if (std::find(sem, sem + d, u) != sem + d) continue;
-            auto& sc = slot_scores[w];
-            if (sc.empty()) {
-                sc.resize(d - half);
-                for (uint32_t sl = half; sl < d; ++sl)
-                    sc[sl - half] = pair_score.at((static_cast<uint64_t>(w) << 32) | sem[sl]);
-            }
-            const size_t weakest = static_cast<size_t>(std::min_element(sc.begin(), sc.end()) - sc.begin());
-            const double incoming = pair_score.at((static_cast<uint64_t>(w) << 32) | u);
+            double* sc = ps.data() + slot_base[w];
+            const size_t weakest = static_cast<size_t>(std::min_element(sc, sc + (d - half)) - sc);
+            const double incoming = ps[edge_pair[i][q]];
             if (incoming > sc[weakest]) {
                 sem[half + weakest] = u;
                 sc[weakest] = incoming;
@@ -491,6 +564,7 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
         }
     }
 
+    mark("reverse slots");
     // ---- keyword and logical edges, entity map, norm order; device refresh
     HostList kw;
     kw.ptr.assign(1, 0);
@@ -523,9 +597,11 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
             ix.lg_ptr_h.push_back(ix.lg_ptr_h.back() + e.size() / 4);
         }
     }
+    mark("keyword/logical/entity map");
     ix.semantic.upload(ix.semantic_h, s);
     ix.norm_order_h.clear();  // rebuild_norm_order (index.cpp:12-23)
     index_finish(ix, &kgv);
+    mark("upload + index_finish");
 }
 
 }  // namespace
@@ -567,6 +643,7 @@ int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p,
 
         auto t0 = Clock::now();
         DevKnn g;
+        HostTimer ht("index_build");
         knn_build_device(*c, p->knn_k, p->knn_iterations, 0.01, p->seed, g, s);
         FGB_CUDA(cudaStreamSynchronize(s));
         ix->build_seconds[0] = secs(t0);
@@ -589,8 +666,10 @@ int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p,
             std::copy(kw.begin() + u * g.k, kw.begin() + u * g.k + kwc[u],
                       ix->keyword_h.idx.begin() + ix->keyword_h.ptr[u]);
         ix->build_seconds[1] = secs(t0);
+        ht.mark("refine");
 
         index_finish(*ix, kg);
+        ht.mark("finish");
         ix->build_seconds[4] = secs(t_all);
         *out = ix.release();
     });

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -40,12 +41,9 @@ struct fg_index {
     uint32_t max_kw_edges = 0, max_logical_group = 0;
     double build_seconds[5] = {0, 0, 0, 0, 0};
 
-    // search scratch, grown on demand and reused across calls
-    fgb::DevBuf<uint32_t> scratch_bits;
-    fgb::DevBuf<uint32_t> scratch_lists;
-    fgb::DevBuf<unsigned char> scratch_misc;
-    uint64_t scratch_slots = 0;
-    fgb::SearchIo io;        // batch_query buffers (one call at a time: search_mu)
+    // search scratch + batch buffers: shared by every index on the device
+    // (fgb::search_workspace), grown on demand, reused across calls
+    std::shared_ptr<fgb::SearchWorkspace> ws;
     std::mutex search_mu;
     double last_kernel_ms = 0.0;
     uint64_t last_launches = 0;
@@ -53,6 +51,9 @@ struct fg_index {
 };
 
 namespace fgb {
+// The device's shared search workspace (created on first use, freed with the
+// last index that holds it).  Callers lock ws->mu around its use.
+std::shared_ptr<SearchWorkspace> search_workspace(int device);
 // Uploads host edge tables into ix (device + host mirrors) and derives the
 // KG adjacency; entity map from the corpus.
 void index_finish(fg_index& ix, const fg_kg_view* kg);

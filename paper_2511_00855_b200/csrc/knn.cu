@@ -1040,7 +1040,9 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
                           double convergence, uint64_t seed, DevKnn& g, cudaStream_t s) {
     uint32_t k = k_req;
     if (c.n >= 2 && k >= c.n) k = static_cast<uint32_t>(c.n - 1);  // knn_graph.cpp:153-156
+    HostTimer ht("knn_build");
     knn_init_device(c, k, seed, g, s);
+    ht.mark("init");
     const double denom = static_cast<double>(c.n) * k;
     uint32_t passes = 0;
     ReverseLists R;
@@ -1048,6 +1050,7 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
     DevBuf<unsigned long long> d_changed;
     for (uint32_t it = 0; it < max_iterations; ++it) {
         const uint64_t changed = knn_iterate_device(c, g, s, R, next, d_changed);
+        ht.mark("pass");
         ++passes;
         if (static_cast<double>(changed) / denom < convergence) break;
     }

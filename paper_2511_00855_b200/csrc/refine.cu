@@ -863,9 +863,13 @@ void refine_merge(uint64_t n, RefineOut& out, cudaStream_t s) {
 
 void refine_device(const fg_corpus& c, const DevKnn& g, uint32_t degree, bool per_neighbour,
                    RefineOut& out, cudaStream_t s) {
+    HostTimer ht("refine");
     refine_alloc(g, degree, out, s);
+    ht.mark("alloc");
     refine_nodes(c, g, per_neighbour, 0, g.n, out, s);
+    ht.mark("nodes");
     refine_merge(g.n, out, s);
+    ht.mark("merge");
 }
 
 }  // namespace fgb

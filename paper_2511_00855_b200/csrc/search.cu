@@ -1027,11 +1027,22 @@ void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg
                     std::vector<std::string>& errs, uint64_t nq, uint32_t stride, cudaStream_t s,
                     double extra_ms = 0.0) {
     (void)q;
-    SearchIo& io = ix->io;
+    SearchIo& io = ix->ws->io;
     // pinned staging: 8-byte fields first, then the 4-byte ones
     const uint64_t hits = nq * stride;
-    io.host.ensure(hits * 12 + nq * 32 + 16);
-    unsigned char* h = io.host.get();
+    const uint64_t bytes = hits * 12 + nq * 32 + 16;
+    // large batches come back through grow-only pinned staging (DMA speed);
+    // small ones through pageable memory — a first cudaMallocHost costs
+    // milliseconds, more than a small batch's whole search (insert_batch)
+    std::vector<unsigned char> small;
+    unsigned char* h = nullptr;
+    if (bytes <= (512u << 10) && io.host.get() == nullptr) {
+        small.resize(bytes);
+        h = small.data();
+    } else {
+        io.host.ensure(bytes);
+        h = io.host.get();
+    }
     double* h_score = reinterpret_cast<double*>(h);
     unsigned long long* h_exp = reinterpret_cast<unsigned long long*>(h_score + hits);
     unsigned long long* h_sc = h_exp + nq;
@@ -1086,7 +1097,11 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         if (!cix || !q || !out) throw Error("invalid-argument", "null pointer");
         fg_index* ix = const_cast<fg_index*>(cix);
         std::lock_guard<std::mutex> lock(ix->search_mu);
+        HostTimer ht("batch_query");
         fg_corpus& c = *ix->corpus;
+        if (!ix->ws) ix->ws = search_workspace(c.device);
+        SearchWorkspace& W = *ix->ws;
+        std::lock_guard<std::mutex> wlock(W.mu);
         FGB_CUDA(cudaSetDevice(c.device));
         cudaStream_t s = c.stream;
         const uint64_t nq = q->count;
@@ -1172,8 +1187,9 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             }
         }
 
+        ht.mark("validate+seeds");
         // ---- device copies of the batch (buffers reused across calls)
-        SearchIo& io = ix->io;
+        SearchIo& io = W.io;
         QueryUpload& up = io.up;
         up.upload(*q, s);
         DevBuf<uint64_t>& d_sptr = io.sptr;
@@ -1203,6 +1219,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         DevBuf<unsigned long long>&r_exp = io.r_exp, &r_sc = io.r_sc;
         io.work.ensure(1);
         FGB_CUDA(cudaMemsetAsync(io.work.get(), 0, sizeof(unsigned int), s));
+        ht.mark("upload");
         DevBuf<unsigned int>& work = io.work;
 
         // ---- plain batches (no entity context, no required keywords): the
@@ -1261,14 +1278,16 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             if (plain_warp_smem(pl) > 0) {
                 const uint64_t slots = plain_slots(pl, nq, c.device);
                 pl.nwords = (n + 31) / 32;
-                pl.tcap = 65536;
-                if (ix->scratch_bits.size() < slots * pl.nwords) {
-                    ix->scratch_bits.alloc(slots * pl.nwords);
-                    ix->scratch_bits.zero(s);
+                // touched-list capacity: a query visits at most n nodes
+                pl.tcap = 1024;
+                while (pl.tcap < 65536 && pl.tcap < n) pl.tcap <<= 1;
+                if (W.bits.size() < slots * pl.nwords) {
+                    W.bits.alloc(slots * pl.nwords);
+                    W.bits.zero(s);
                 }
-                pl.visited = ix->scratch_bits.get();
-                ix->scratch_lists.ensure(slots * pl.tcap);
-                pl.touched = ix->scratch_lists.get();
+                pl.visited = W.bits.get();
+                W.lists.ensure(slots * pl.tcap);
+                pl.touched = W.lists.get();
                 pl.hit_stride = stride;
                 pl.r_node = r_node.get();
                 pl.r_score = r_score.get();
@@ -1292,9 +1311,11 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                     stats.zero(s);
                     pl.stats = stats.get();
                 }
+                ht.mark("plain scratch");
                 FGB_CUDA(cudaEventRecord(ix->ev0, s));
                 launch_search_plain(pl, nq, c.device, s);
                 FGB_CUDA(cudaEventRecord(ix->ev1, s));
+                ht.mark("plain kernel");
                 if (pl.timing || pl.stats) {
                     unsigned long long t[kPlainPhCount] = {}, st[2] = {};
                     if (pl.timing) timing.download(t, kPlainPhCount, s);
@@ -1320,6 +1341,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                                      st[0], st[1]);
                 }
                 finish_results(ix, c, q, out, errs, nq, stride, s);
+                ht.mark("results");
                 ix->last_launches = 1;
                 return;
             }
@@ -1433,22 +1455,22 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         const uint64_t slots = blocks * kWarpsPerBlock;
         const uint64_t nbitsets = 1 + (any_ctx ? 1 : 0) + (any_req ? 1 : 0);
         const uint64_t bits_words = slots * a.nwords * nbitsets;
-        if (ix->scratch_bits.size() < bits_words) {
-            ix->scratch_bits.alloc(bits_words);
-            ix->scratch_bits.zero(s);
+        if (W.bits.size() < bits_words) {
+            W.bits.alloc(bits_words);
+            W.bits.zero(s);
         }
-        uint32_t* bits = ix->scratch_bits.get();
+        uint32_t* bits = W.bits.get();
         a.visited = bits;
         a.expbits = any_ctx ? bits + slots * a.nwords : nullptr;
         a.twinbits = any_req ? bits + slots * a.nwords * (any_ctx ? 2 : 1) : nullptr;
         const uint64_t list_words = slots * (a.tcap + a.twcap);
-        ix->scratch_lists.ensure(std::max<uint64_t>(list_words, 1));
-        a.touched = ix->scratch_lists.get();
+        W.lists.ensure(std::max<uint64_t>(list_words, 1));
+        a.touched = W.lists.get();
         a.twin_node = any_req ? a.touched + slots * a.tcap : nullptr;
         const uint64_t misc = slots * (static_cast<uint64_t>(a.twcap) * 8 + static_cast<uint64_t>(a.ctxcap) * 16);
-        ix->scratch_misc.ensure(std::max<uint64_t>(misc, 16));
-        a.twin_raw = any_req ? reinterpret_cast<double*>(ix->scratch_misc.get()) : nullptr;
-        a.ctx = any_ctx ? reinterpret_cast<uint4*>(ix->scratch_misc.get() + slots * a.twcap * 8) : nullptr;
+        W.misc.ensure(std::max<uint64_t>(misc, 16));
+        a.twin_raw = any_req ? reinterpret_cast<double*>(W.misc.get()) : nullptr;
+        a.ctx = any_ctx ? reinterpret_cast<uint4*>(W.misc.get() + slots * a.twcap * 8) : nullptr;
         if (any_ctx) FGB_CUDA(cudaMemsetAsync(a.ctx, 0xFF, slots * a.ctxcap * 16, s));
         a.hit_stride = stride;
         a.r_node = r_node.get();

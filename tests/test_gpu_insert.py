@@ -63,3 +63,34 @@ def test_insert_rejects_duplicates_untouched(split):
         gix.insert(part(c, np.array([650, 650])))        # repeated within the batch
     assert e.value.code == "duplicate-id"
     same(gix.export(), before)
+
+
+def test_insert_cost_at_scale():
+    """acceptance.cpp:523-572 at the bench's row shape (d=768, learned nnz
+    120, knn_k 64, degree 32), where cost rather than launch latency decides:
+    insert 20% of a 100K-doc corpus into an index of the other 80% vs a
+    rebuild of all of it — insert time under 40% of the rebuild's, recall@10
+    (beam 128) within 0.02 of the rebuild's."""
+    import time
+    p = A.synth_params(docs=100000, dense_dim=768, clusters=20, cluster_spread=0.25, learned_vocab=30522,
+                       learned_nnz=120, statistical_vocab=0, statistical_nnz=40, seed=61)
+    c, kg, _ = synth.generate_corpus(p, 0)
+    n0 = 80000
+    build = dict(degree=32, knn_k=64, seed=6100)
+    fg.build_hybrid_index(fg.DeviceCorpus(part(c, np.arange(4000))), kg, **build).close()  # warm-up
+    t0 = time.perf_counter()
+    full = fg.build_hybrid_index(fg.DeviceCorpus(c), kg, **build)
+    rebuild_s = time.perf_counter() - t0
+    inc = fg.build_hybrid_index(fg.DeviceCorpus(part(c, np.arange(n0))), kg, **build)
+    extra = part(c, np.arange(n0, c.n))  # prepared before the clock, as acceptance.cpp:546-548
+    t0 = time.perf_counter()
+    inc.insert(extra)
+    insert_s = time.perf_counter() - t0
+    q = synth.synth_queries(p, 200, beam_width=128)
+    truth = fg.brute_force_topk(full.corpus, q)
+    rf, ri = fg.batch_query(full, q), fg.batch_query(inc, q)
+    rec = lambda r: np.mean([fg.recall_at_k(r.ids(i), truth.ids(i), 10) for i in range(q.count)])
+    print(f"rebuild {rebuild_s:.3f}s insert {insert_s:.3f}s ({100 * insert_s / rebuild_s:.0f}%), "
+          f"recall rebuild {rec(rf):.4f} insert {rec(ri):.4f}")
+    assert rec(ri) >= rec(rf) - 0.02
+    assert insert_s < 0.40 * rebuild_s
