@@ -382,6 +382,10 @@ int fg_brute_force_topk(const fg_corpus* c, const fg_query_view* q, fg_search_re
  * and the number of kernel launches it issued. */
 int fg_last_search_stats(const fg_index* ix, double* kernel_ms, uint64_t* launches);
 
+/* Name of the kernel the last fg_batch_query ran ("search_plain_kernel",
+ * "search_hybrid_kernel" or "search_kernel"; "" before the first call). */
+int fg_last_search_kernel(const fg_index* ix, const char** name);
+
 /* Diagnostics of the refinery's tensor-core candidate Gram (refine.cu,
  * gram_tc_*; replaces the dense half of candidate_pair_scores,
  * refine.cpp:11-23, with a certified split-bf16 tcgen05 product): pairs

@@ -77,6 +77,7 @@ def _declare(lib):
                                      P(A.SearchResults)]),
         "fg_brute_force_topk": (C.c_int, [C.c_void_p, P(A.QueryView), P(A.SearchResults)]),
         "fg_last_search_stats": (C.c_int, [C.c_void_p, A.f64p, A.u64p]),
+        "fg_last_search_kernel": (C.c_int, [C.c_void_p, C.POINTER(C.c_char_p)]),
         "fg_refine_tc_stats": (C.c_int, [A.u64p, A.u64p, A.f64p, C.c_int]),
     }
     missing = []

@@ -211,6 +211,7 @@ struct SearchIo {
     DevBuf<uint64_t> sptr;
     DevBuf<uint32_t> snode, sent;
     DevBuf<uint8_t> shas, qflags;
+    DevBuf<double> rew;  // per entity query: w_k / hop (hybrid kernel)
     DevBuf<uint32_t> r_node, r_count, r_warn, r_err;
     DevBuf<double> r_score;
     DevBuf<unsigned long long> r_exp, r_sc;

@@ -46,6 +46,7 @@ struct fg_index {
     std::shared_ptr<fgb::SearchWorkspace> ws;
     std::mutex search_mu;
     double last_kernel_ms = 0.0;
+    const char* last_kernel = "";
     uint64_t last_launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };

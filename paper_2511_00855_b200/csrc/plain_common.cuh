@@ -27,6 +27,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7FF0000000000000ll); }
 
+// An upper bound of sqrt(x) (x >= 0) without the fp64 sqrt's out-of-line
+// slow path: fp32 rounded up, MUFU sqrt, widened by 2^-18 (> its error).
+__device__ __forceinline__ double sqrt_ub(double x) {
+    const float f = __double2float_ru(x);
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(f));
+    return static_cast<double>(r) * (1.0 + 0x1p-18) + 1e-300;
+}
+// (The search kernels avoid every out-of-line call — fp64 sqrt and division
+// have one — because ptxas 12.9 for sm_100a clobbered live registers around
+// such calls in these large kernels.)
+
 __device__ __forceinline__ bool eless(double d1, uint32_t n1, double d2, uint32_t n2) {
     return d1 < d2 || (d1 == d2 && n1 < n2);  // entry_less (search.cpp:13-16)
 }
@@ -43,16 +55,42 @@ struct QueryQ {
 
 // The reference's exact distance — the sequential chains of
 // scoring.cpp:10-99 (dense in index order, then each sparse path's shared
-// terms in ascending order; products of fp32 values exact in fp64, one
-// rounding per add).  The rare path (uncertain comparisons, final top-k).
+// terms in ascending order; products of fp32 values exact in fp64, so one
+// FMA per term rounds exactly like the reference's `acc += a * b`).  The rare
+// path (uncertain comparisons, top-k entries).  Rows stream as 16-byte loads
+// kept 8 (dense) / 2 groups (sparse) ahead of the chain; the zero padding of
+// dense rows and the (kPad, 0) padding of posting groups add nothing.
 // (Kept inline: an out-of-line call here corrupted live batch registers
 // under sm_100a ptxas 12.9 — tools/smoke_plain.py reproduced it.)
 __device__ __forceinline__ double exact_dist(const DevCorpus& c, const QueryQ& Q, uint32_t node) {
     double acc = 0.0;
     if (Q.qd) {
-        const float* row = c.dense + static_cast<uint64_t>(node) * c.dstride;
-        for (uint32_t i = 0; i < c.dstride; ++i)
-            acc = __dadd_rn(acc, __dmul_rn((double)Q.qd[i], (double)row[i]));
+        constexpr uint32_t S = 8;
+        const float4* row = reinterpret_cast<const float4*>(c.dense + static_cast<uint64_t>(node) * c.dstride);
+        const float4* q4 = reinterpret_cast<const float4*>(Q.qd);
+        const uint32_t n4 = c.dstride >> 2;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 cur[S];
+#pragma unroll
+        for (uint32_t j = 0; j < S; ++j) cur[j] = j < n4 ? __ldg(row + j) : z;
+#pragma unroll 1
+        for (uint32_t i = 0; i < n4; i += S) {
+            float4 nxt[S];
+#pragma unroll
+            for (uint32_t j = 0; j < S; ++j) nxt[j] = i + S + j < n4 ? __ldg(row + i + S + j) : z;
+#pragma unroll
+            for (uint32_t j = 0; j < S; ++j) {
+                if (i + j < n4) {
+                    const float4 q = q4[i + j];
+                    acc = __fma_rn((double)q.x, (double)cur[j].x, acc);
+                    acc = __fma_rn((double)q.y, (double)cur[j].y, acc);
+                    acc = __fma_rn((double)q.z, (double)cur[j].z, acc);
+                    acc = __fma_rn((double)q.w, (double)cur[j].w, acc);
+                }
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < S; ++j) cur[j] = nxt[j];
+        }
     }
 #pragma unroll 1
     for (int path = 0; path < 2; ++path) {
@@ -61,13 +99,43 @@ __device__ __forceinline__ double exact_dist(const DevCorpus& c, const QueryQ& Q
         const PathQ P = learned ? Q.p[0] : Q.p[1];
         if (P.on) {
             const uint64_t off = learned ? c.l_off[node] : c.s_off[node];
-            const uint32_t nnz = learned ? c.l_nnz[node] : c.s_nnz[node];
-            const uint32_t* idx = (learned ? c.l_idx : c.s_idx) + off;
-            const float* val = (learned ? c.l_val : c.s_val) + off;
-            for (uint32_t j = 0; j < nnz; ++j) {
-                bool f;
-                const float q = q_lookup(P, idx[j], f);
-                if (f) s = __dadd_rn(s, __dmul_rn((double)q, (double)val[j]));
+            const uint32_t n4 = ((learned ? c.l_nnz[node] : c.s_nnz[node]) + 3) >> 2;
+            const uint4* i4 = reinterpret_cast<const uint4*>((learned ? c.l_idx : c.s_idx) + off);
+            const float4* v4 = reinterpret_cast<const float4*>((learned ? c.l_val : c.s_val) + off);
+            const uint4 pi = make_uint4(kPad, kPad, kPad, kPad);
+            const float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint4 ci[2];
+            float4 cv[2];
+#pragma unroll
+            for (uint32_t j = 0; j < 2; ++j) {
+                ci[j] = j < n4 ? __ldg(i4 + j) : pi;
+                cv[j] = j < n4 ? __ldg(v4 + j) : pv;
+            }
+#pragma unroll 1
+            for (uint32_t g = 0; g < n4; g += 2) {
+                uint4 ni[2];
+                float4 nv[2];
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j) {
+                    ni[j] = g + 2 + j < n4 ? __ldg(i4 + g + 2 + j) : pi;
+                    nv[j] = g + 2 + j < n4 ? __ldg(v4 + g + 2 + j) : pv;
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j) {
+                    const uint32_t t[4] = {ci[j].x, ci[j].y, ci[j].z, ci[j].w};
+                    const float v[4] = {cv[j].x, cv[j].y, cv[j].z, cv[j].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        bool f;
+                        const float q = q_lookup(P, t[e], f);
+                        if (f) s = __fma_rn((double)q, (double)v[e], s);
+                    }
+                }
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j) {
+                    ci[j] = ni[j];
+                    cv[j] = nv[j];
+                }
             }
         }
         acc = __dadd_rn(acc, s);

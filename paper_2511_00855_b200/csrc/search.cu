@@ -33,6 +33,7 @@
 #include "fg_cuda.hpp"
 #include "index.hpp"
 #include "query_stage.cuh"
+#include "search_hybrid.hpp"
 #include "search_plain.hpp"
 #include "tma.cuh"
 
@@ -1084,6 +1085,163 @@ void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg
         }
     }
 }
+// Entity-context / required-keyword batches on the certified kernel
+// (search_hybrid.cu).  Queries that overflow their twin pool or context table
+// are re-run alone with 4x larger tables; false when the batch does not fit
+// the kernel's shared memory (the caller falls back to search_kernel).
+bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunch& pl, const fg_query_view* q,
+                const std::vector<uint8_t>& qflags, uint32_t max_seeds, uint32_t max_req, bool any_ctx,
+                bool any_req, bool conj,
+                uint64_t nq, uint32_t stride, std::vector<std::string>& errs, fg_search_results* out,
+                cudaStream_t s) {
+    SearchIo& io = W.io;
+    const uint64_t n = c.n;
+    HybridLaunch h{};
+    h.p = pl;
+    h.seed_ptr = io.sptr.get();
+    h.seed_node = io.snode.get();
+    h.seed_ent = io.sent.get();
+    // rewards w_k / hop (search.cpp:156-161) divided here, in the
+    // reference's double arithmetic: the kernel does no fp64 division
+    if (any_ctx) {
+        uint32_t hmax = 1;
+        for (uint64_t i = 0; i < nq; ++i)
+            if (qflags[i] & QF_ENTITY)
+                hmax = std::max(hmax, q->max_entity_hops ? q->max_entity_hops[i] : 2u);
+        if (hmax > 4096) return false;  // (the exact-chain kernel divides on the device)
+        h.rstride = hmax;
+        std::vector<double> tab(nq * hmax, 0.0);
+        for (uint64_t i = 0; i < nq; ++i)
+            if (qflags[i] & QF_ENTITY) {
+                const double went = static_cast<double>(q->weights[i].entity);
+                for (uint32_t hop = 1; hop <= hmax; ++hop) tab[i * hmax + hop - 1] = went / static_cast<double>(hop);
+            }
+        io.rew.upload(tab, s);
+        h.rewards = io.rew.get();
+    }
+    h.kw_ptr = ix->kw_ptr.get();
+    h.kw_idx = ix->kw_idx.get();
+    h.lg_ptr = ix->lg_ptr.get();
+    h.lg = ix->lg.get();
+    h.kg_ptr = ix->kg_ptr.get();
+    h.kg_nbr = ix->kg_nbr.get();
+    h.kg_rows = ix->kg_rows;
+    h.conjunctive = conj ? 1 : 0;
+    h.reqcap = std::max(max_req, 1u);
+    h.lccap = std::max(ix->max_logical_group, 1u);
+    const uint32_t list_max = ix->degree + (any_req ? ix->max_kw_edges : 0) + (any_ctx ? h.lccap : 0);
+    h.seencap = 64;
+    while (h.seencap < 2 * list_max) h.seencap <<= 1;
+    if (hybrid_warp_smem(h) == 0) return false;
+    const uint64_t all_slots = hybrid_slots(h, nq, c.device);
+    h.p.hit_stride = stride;
+    h.p.r_node = io.r_node.get();
+    h.p.r_score = io.r_score.get();
+    h.p.r_count = io.r_count.get();
+    h.p.r_expanded = io.r_exp.get();
+    h.p.r_scored = io.r_sc.get();
+    h.p.r_warn = io.r_warn.get();
+    h.p.r_err = io.r_err.get();
+    h.p.work = io.work.get();
+    h.p.timing = nullptr;
+    h.p.nwords = (n + 31) / 32;
+    h.p.tcap = 1024;
+    while (h.p.tcap < 65536 && h.p.tcap < n) h.p.tcap <<= 1;
+    uint32_t twcap0 = any_req ? 4096 : 0, ctxcap0 = 0;
+    if (any_ctx) {
+        ctxcap0 = 8192;
+        while (ctxcap0 < 4ull * max_seeds && ctxcap0 < (1u << 26)) ctxcap0 <<= 1;
+    }
+    if (const char* e = std::getenv("FGB_SEARCH_SCRATCH0")) {  // test hook: force re-runs
+        const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+        if (v >= 2 && (v & (v - 1)) == 0) {
+            if (any_req) twcap0 = v;
+            if (any_ctx) ctxcap0 = v;
+        }
+    }
+    DevBuf<unsigned long long> stats;
+    const char* se = std::getenv("FGB_SEARCH_STATS");
+    if ((se && se[0] == '1') || h.p.eps_scale != 1.0) {
+        stats.alloc(2);
+        stats.zero(s);
+        h.p.stats = stats.get();
+    }
+    DevBuf<unsigned long long> timing;
+    if (const char* te = std::getenv("FGB_SEARCH_TIMING"); te && te[0] == '1') {
+        timing.alloc(kHybCount);
+        timing.zero(s);
+        h.timing = timing.get();
+    }
+    std::vector<uint32_t> rerun;
+    DevBuf<uint32_t> d_rerun;
+    float ms_prev = 0.f;
+    for (int attempt = 0;; ++attempt) {
+        h.twcap = twcap0 << (2 * attempt);
+        h.ctxcap = ctxcap0 << (2 * attempt);
+        const uint64_t slots = attempt ? std::min<uint64_t>(all_slots, rerun.size()) : all_slots;
+        const uint64_t nbits = 1 + (any_ctx ? 1 : 0) + (any_req ? 1 : 0);
+        const uint64_t bits_words = slots * h.p.nwords * nbits;
+        if (W.bits.size() < bits_words) {
+            W.bits.alloc(bits_words);
+            W.bits.zero(s);
+        }
+        uint32_t* bits = W.bits.get();
+        h.p.visited = bits;
+        h.expbits = any_ctx ? bits + slots * h.p.nwords : nullptr;
+        h.twinbits = any_req ? bits + slots * h.p.nwords * (any_ctx ? 2 : 1) : nullptr;
+        W.lists.ensure(std::max<uint64_t>(slots * (static_cast<uint64_t>(h.p.tcap) + h.twcap), 1));
+        h.p.touched = W.lists.get();
+        h.twin_node = any_req ? h.p.touched + slots * h.p.tcap : nullptr;
+        const uint64_t misc = slots * (static_cast<uint64_t>(h.twcap) * 8 + static_cast<uint64_t>(h.ctxcap) * 16);
+        W.misc.ensure(std::max<uint64_t>(misc, 16));
+        h.twin_d = any_req ? reinterpret_cast<double*>(W.misc.get()) : nullptr;
+        h.ctx = any_ctx ? reinterpret_cast<uint4*>(W.misc.get() + slots * h.twcap * 8) : nullptr;
+        if (any_ctx) FGB_CUDA(cudaMemsetAsync(h.ctx, 0xFF, slots * h.ctxcap * 16, s));
+        h.qlist = attempt ? d_rerun.get() : nullptr;
+        h.qlist_n = static_cast<uint32_t>(rerun.size());
+        FGB_CUDA(cudaMemsetAsync(h.p.work, 0, sizeof(unsigned int), s));
+        FGB_CUDA(cudaEventRecord(ix->ev0, s));
+        launch_search_hybrid(h, slots, s);
+        FGB_CUDA(cudaEventRecord(ix->ev1, s));
+        ix->last_launches = attempt + 1;
+        ix->last_kernel = "search_hybrid_kernel";
+        std::vector<uint32_t> h_err(nq);
+        io.r_err.download(h_err.data(), nq, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        rerun.clear();
+        for (uint64_t i = 0; i < nq; ++i)
+            if (h_err[i]) rerun.push_back(static_cast<uint32_t>(i));
+        constexpr uint64_t kMaxScratch = 1ull << 30;  // bytes of twin + context tables per launch
+        const uint64_t next_slots = std::min<uint64_t>(all_slots, rerun.size());
+        const uint64_t next_bytes = next_slots * ((uint64_t(h.twcap) * 12 + uint64_t(h.ctxcap) * 16) << 2);
+        if (rerun.empty() || next_bytes > kMaxScratch) break;
+        float ms = 0;
+        FGB_CUDA(cudaEventElapsedTime(&ms, ix->ev0, ix->ev1));
+        ms_prev += ms;
+        d_rerun.upload(rerun, s);
+    }
+    if (h.p.stats) {
+        unsigned long long st[2] = {};
+        stats.download(st, 2, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[hybrid stats] exact resolutions %llu, exact final entries %llu\n", st[0], st[1]);
+    }
+    if (h.timing) {
+        unsigned long long t[kHybCount] = {};
+        timing.download(t, kHybCount, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        const double X = t[kHybExpanded] ? (double)t[kHybExpanded] : 1.0;
+        static const char* names[] = {"select+lists", "gather+dedupe", "visited+ctx", "sparse", "dense",
+                                      "cand certify", "top-k", "final"};
+        std::fprintf(stderr, "[hybrid timing] %llu queries, %.1f expansions/query, %.2f batches/expansion\n",
+                     t[kHybQueries], X / std::max(1ull, t[kHybQueries]), t[kHybBatches] / X);
+        for (int k = 0; k < kHybPhases; ++k)
+            std::fprintf(stderr, "  %-16s %10.0f cycles/expansion\n", names[k], t[k] / X);
+    }
+    finish_results(ix, c, q, out, errs, nq, stride, s, ms_prev);
+    return true;
+}
+
 }  // namespace
 }  // namespace fgb
 
@@ -1224,9 +1382,15 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
 
         // ---- plain batches (no entity context, no required keywords): the
         // certified-approximate kernel (search_plain.cu), bit-identical results
+        // Entity-context / required-keyword batches: the certified kernel of
+        // search_hybrid.cu (FGB_SEARCH_HYBRID=0: the exact-chain search_kernel)
         const char* pe = std::getenv("FGB_SEARCH_PLAIN");
-        const bool plain_ok = !any_ctx && !any_req && (!pe || pe[0] != '0') && n < kId30 && c.dc.meta && ix->edge_meta.get();
-        if (plain_ok && nq) {
+        const char* he = std::getenv("FGB_SEARCH_HYBRID");
+        const char* fe = std::getenv("FGB_SEARCH_FORCE_HYBRID");  // dev A/B: plain batches on the hybrid kernel
+        const bool special = any_ctx || any_req || (fe && fe[0] == '1');
+        const bool cert_ok = (!pe || pe[0] != '0') && (!special || !he || he[0] != '0') && n < kId30 && c.dc.meta &&
+                             ix->edge_meta.get();
+        if (cert_ok && nq) {
             PlainLaunch pl{};
             pl.c = c.dc;
             pl.semantic = ix->semantic.get();
@@ -1275,7 +1439,10 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             // the first (4: +2% at 1M docs)
             pl.prefetch = 5;
             if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) pl.prefetch = std::atoi(e);
-            if (plain_warp_smem(pl) > 0) {
+            if (special) {
+                if (run_hybrid(ix, c, W, pl, q, qflags, max_seeds, max_req, any_ctx, any_req, conj, nq, stride, errs, out, s))
+                    return;
+            } else if (plain_warp_smem(pl) > 0) {
                 const uint64_t slots = plain_slots(pl, nq, c.device);
                 pl.nwords = (n + 31) / 32;
                 // touched-list capacity: a query visits at most n nodes
@@ -1343,6 +1510,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                 finish_results(ix, c, q, out, errs, nq, stride, s);
                 ht.mark("results");
                 ix->last_launches = 1;
+                ix->last_kernel = "search_plain_kernel";
                 return;
             }
         }
@@ -1489,6 +1657,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
         FGB_LAUNCH("search_kernel");
         FGB_CUDA(cudaEventRecord(ix->ev1, s));
         ix->last_launches = nq ? attempt + 1 : 0;
+        ix->last_kernel = "search_kernel";
         // overflowed queries: re-run them alone with larger scratch
         constexpr uint64_t kMaxScratch = 1ull << 30;  // bytes of twin + context tables per launch
         std::vector<uint32_t> h_err(nq);
@@ -1523,6 +1692,13 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                          t[kPhLaneDense] / std::max(1.0, (double)t[kPhLaneDenseRows]),
                          t[kPhLaneScored], t[kPhLaneDenseRows]);
         }
+    });
+}
+
+int fg_last_search_kernel(const fg_index* ix, const char** name) {
+    return guarded([&] {
+        if (!ix || !name) throw Error("invalid-argument", "null pointer");
+        *name = ix->last_kernel;
     });
 }
 

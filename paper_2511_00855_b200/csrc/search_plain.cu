@@ -140,12 +140,12 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             qd2 += __shfl_xor_sync(kFull, qd2, o);
             qs2 += __shfl_xor_sync(kFull, qs2, o);
         }
-        const double qnorm = sqrt(qd2) * (1.0 + 1e-12);
+        const double qnorm = sqrt_ub(qd2);
         // |approx - reference| <= eps: fp32 dense partials (gamma_4 in fp32 of
         // sum |q_i d_i| <= |q_d| max|d_dense|) + fp64 sums (depths N, M) of all
         // products (sum |p| <= |q_w| max|d|, Cauchy-Schwarz)
-        const double eps = (a.eps32_coef * (sqrt(qd2) * (1.0 + 1e-10)) * a.max_dnorm +
-                            a.eps_coef * (sqrt(qd2 + qs2) * (1.0 + 1e-10)) * a.max_norm) * a.eps_scale + 1e-300;
+        const double eps = (a.eps32_coef * qnorm * a.max_dnorm + a.eps_coef * sqrt_ub(qd2 + qs2) * a.max_norm) *
+                               a.eps_scale + 1e-300;
         const double tol = 2.5 * eps;
 
         const Pool topk{w.topk_d, w.topk_n, K};

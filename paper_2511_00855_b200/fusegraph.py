@@ -232,6 +232,11 @@ class HybridIndex:
         check(lib().fg_last_search_stats(self.h, C.byref(ms), C.byref(launches)))
         return ms.value, launches.value
 
+    def last_search_kernel(self) -> str:
+        name = C.c_char_p()
+        check(lib().fg_last_search_kernel(self.h, C.byref(name)))
+        return name.value.decode()
+
 
 def build_hybrid_index(dc: DeviceCorpus, kg: A.KG | None = None, degree=32, knn_k=32,
                        knn_iterations=10, seed=42, logical_cap=64, default_entity_hops=2,

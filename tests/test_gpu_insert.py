@@ -78,14 +78,17 @@ def test_insert_cost_at_scale():
     n0 = 80000
     build = dict(degree=32, knn_k=64, seed=6100)
     fg.build_hybrid_index(fg.DeviceCorpus(part(c, np.arange(4000))), kg, **build).close()  # warm-up
-    t0 = time.perf_counter()
-    full = fg.build_hybrid_index(fg.DeviceCorpus(c), kg, **build)
-    rebuild_s = time.perf_counter() - t0
-    inc = fg.build_hybrid_index(fg.DeviceCorpus(part(c, np.arange(n0))), kg, **build)
-    extra = part(c, np.arange(n0, c.n))  # prepared before the clock, as acceptance.cpp:546-548
-    t0 = time.perf_counter()
-    inc.insert(extra)
-    insert_s = time.perf_counter() - t0
+    base, extra = part(c, np.arange(n0)), part(c, np.arange(n0, c.n))  # prepared before the clocks
+    rebuild_s, insert_s = [], []
+    for _ in range(2):  # best of two of each (shared-host timing noise)
+        t0 = time.perf_counter()
+        full = fg.build_hybrid_index(fg.DeviceCorpus(c), kg, **build)
+        rebuild_s.append(time.perf_counter() - t0)
+        inc = fg.build_hybrid_index(fg.DeviceCorpus(base), kg, **build)
+        t0 = time.perf_counter()
+        inc.insert(extra)  # acceptance.cpp:546-548
+        insert_s.append(time.perf_counter() - t0)
+    rebuild_s, insert_s = min(rebuild_s), min(insert_s)
     q = synth.synth_queries(p, 200, beam_width=128)
     truth = fg.brute_force_topk(full.corpus, q)
     rf, ri = fg.batch_query(full, q), fg.batch_query(inc, q)

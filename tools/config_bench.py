@@ -149,6 +149,10 @@ def main():
             cq = A.Queries(dense, learned, stat, w, k=10, beam_width=128, max_entity_hops=2,
                            entities=ents).pinned()
             cr, ck, cw, cl = timed(ix, cq, 32, a.steps)
+            kname = ix.last_search_kernel()
+            os.environ["FGB_SEARCH_HYBRID"] = "0"  # A/B: the exact-chain search_kernel
+            _, ck0, _, _ = timed(ix, cq, 32, a.steps)
+            del os.environ["FGB_SEARCH_HYBRID"]
             rec = float(np.mean([fg.recall_at_k(cr.ids(i), chains[i].answer_docs, 10) for i in range(len(chains))]))
             key = f"chain_queries_wk{int(went)}"
             gpu_chain[key] = (cq, cr)
@@ -160,6 +164,8 @@ def main():
                         "h2d_bytes_per_step": int(cq.h2d_bytes()), "d2h_bytes_per_step": int(len(chains) * 232)},
                 "roofline": roofline(cr, cq, ck, R, deg),
                 "expanded_per_query": round(float(cr.expanded.mean()), 1),
+                "kernel": kname,
+                "value_search_kernel": round(len(chains) / (statistics.mean(ck0) / 1e3), 1),
                 "queries_with_warnings": int(np.count_nonzero(cr.warnings))}
         line["kg"] = {"triplets": int(len(kg.source)), "chains": len(chains)}
 
@@ -171,6 +177,10 @@ def main():
         kq.required = A.CSR.from_rows([kq.statistical.row(i)[0][:1].tolist() for i in range(kq.count)])
         kq = kq.pinned()
         kr, kk, kw, kl = timed(ix, kq, entry, a.steps)
+        kname = ix.last_search_kernel()
+        os.environ["FGB_SEARCH_HYBRID"] = "0"
+        _, kk0, _, _ = timed(ix, kq, entry, a.steps)
+        del os.environ["FGB_SEARCH_HYBRID"]
         gpu_chain["keyword_queries"] = (kq, kr)
         line["keyword_queries"] = {
             "queries": kq.count, "beam": beam, "entry": entry, "required": "first statistical term, conjunctive",
@@ -178,6 +188,8 @@ def main():
             "e2e": {"value": round(kq.count / statistics.mean(kw), 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(kq.h2d_bytes()), "d2h_bytes_per_step": int(kq.count * 232)},
             "roofline": roofline(kr, kq, kk, R, deg),
+            "kernel": kname,
+            "value_search_kernel": round(kq.count / (statistics.mean(kk0) / 1e3), 1),
             "queries_with_shortfall": int(np.count_nonzero(kr.warnings & 2))}
     if not a.no_cpu:
         from oracle.refpy import RefLib, ref_available
