@@ -214,10 +214,9 @@ __device__ __forceinline__ double reduce_scatter(double (&x)[R], uint32_t lane) 
 // Warp-cooperative approximate dense dot (coalesced 512-B loads per warp
 // instruction) for every lane-held node in `mask`, dense_rows<NQ4>() rows
 // per round trip; fp32 partials of 4 elements, accumulated in fp64.
-template <int NQ4>
+template <int NQ4, int R = dense_rows<NQ4>()>
 __device__ __forceinline__ double dense_group(const DevCorpus& c, const float* qd, uint32_t node, uint32_t lane,
                                               uint32_t mask) {
-    constexpr int R = dense_rows<NQ4>();
     double mine = 0.0;
     const float4* q4 = reinterpret_cast<const float4*>(qd);
     const uint32_t n4 = c.dstride >> 2;

@@ -28,7 +28,7 @@
 namespace fgb {
 namespace {
 
-constexpr int kPassThreads = 512;
+constexpr int kPassThreads = 256;  // two CTAs per SM (launch bound below)
 // Candidates scored between two merges grow 1, 2, then kSRounds batches of
 // kPassThreads (the first merges raise the screening threshold of a random
 // initial list quickly; later rounds amortise the merge's barriers).
@@ -134,6 +134,9 @@ struct PassArgs {
     unsigned long long* timing;
     int prefetch;       // L2 prefetch of the postings of the sparse groups after the first
     uint32_t sort_min;  // entering batches larger than this certify sorted
+    uint32_t nparts;    // the two-hop pool is processed in nparts hash parts (power of two)
+    uint32_t pshift;    // part of id = (id * 0x9E3779B1) >> pshift
+    unsigned int* overflow;  // pool overflow counter (0 after a correct pass)
 };
 
 enum : int {
@@ -141,15 +144,20 @@ enum : int {
     kKnCand, kKnDense, kKnEnter, kKnRounds, kKnResolved, kKnCount   // counters
 };
 
+// Probes are bounded: a full table (a part far above its expected size)
+// raises *overflow and the host fails the build loudly instead of spinning.
 __device__ __forceinline__ void pool_insert(uint32_t* keys, uint32_t* fbits, uint32_t mask,
-                                            uint32_t id, bool fresh) {
+                                            uint32_t id, bool fresh, uint32_t cap, unsigned int* overflow) {
     uint32_t s = hslot(id, mask);
-    while (true) {
+    for (uint32_t probe = 0; probe < cap; ++probe) {
         const uint32_t prev = atomicCAS(&keys[s], kEmpty, id);
-        if (prev == kEmpty || prev == id) break;
+        if (prev == kEmpty || prev == id) {
+            if (fresh) atomicOr(&fbits[s >> 5], 1u << (s & 31));
+            return;
+        }
         s = (s + 1) & mask;
     }
-    if (fresh) atomicOr(&fbits[s >> 5], 1u << (s & 31));
+    atomicAdd(overflow, 1u);
 }
 
 // Exact scores (hybrid_score's arithmetic, element order unchanged) of the
@@ -387,7 +395,7 @@ __device__ void merge_certify_sorted(const PassArgs& a, const SmemQuery& sq, uin
 // get the exact chain.  NQ4 == 0 (dense rows > 1,024 floats): exact chains,
 // thread per candidate.
 template <int NQ4>
-__global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
     const uint64_t u = a.lo + blockIdx.x;
@@ -413,7 +421,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     uint8_t* T_mk = S_ex + kSCap;
     uint8_t* S_mk = T_mk + k;
     __shared__ uint32_t S_cnt, n_mark, t_marked;
-    const uint32_t mask = a.pool_cap - 1;
     long long t_mark = (a.timing && threadIdx.x == 0) ? clock64() : 0;
     auto lap = [&](int ph) {
         if (a.timing && threadIdx.x == 0) {
@@ -426,11 +433,6 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         if (a.timing && v) atomicAdd(&a.timing[slot], static_cast<unsigned long long>(v));
     };
 
-    for (uint32_t j = tid; j < a.pool_cap; j += nt) keys[j] = kEmpty;
-    for (uint32_t j = tid; j < a.pool_cap / 32; j += nt) {
-        fbits[j] = 0;
-        hbits[j] = 0;
-    }
     for (uint32_t j = tid; j < k; j += nt) {
         T_id[j] = a.L_ids[u * k + j];
         T_sc[j] = a.L_sc[u * k + j];
@@ -439,63 +441,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     }
     if (tid == 0) S_cnt = 0;
     stage_doc(a.c, u, smem, a.lcap, a.scap, tid, nt, sq, [] { __syncthreads(); });
-
-    // L[u] members: mark as "have" (their scores are known; knn_graph.cpp:122-131)
-    for (uint32_t j = tid; j < k; j += nt) {
-        const uint32_t id = T_id[j];
-        uint32_t s = hslot(id, mask);
-        while (true) {
-            const uint32_t prev = atomicCAS(&keys[s], kEmpty, id);
-            if (prev == kEmpty || prev == id) break;
-            s = (s + 1) & mask;
-        }
-        atomicOr(&hbits[s >> 5], 1u << (s & 31));
-    }
-    __syncthreads();
     lap(kKnPhInit);
-
-    // Two-hop pool through forward + reverse adjacency (knn_graph.cpp:97-110).
-    // u's first hops (forward list, then reverse list) are staged in shared
-    // memory (the candidate buffers are free until scoring); each thread then
-    // has kHopU second-hop loads in flight before its inserts (the pool is a
-    // set with OR-ed freshness, so insertion order does not matter).
-    const uint32_t rc_u = a.R_cnt[u];
-    const uint32_t nh1 = k + rc_u;
-    uint32_t* hop_id = S_id;
-    uint32_t* hop_rc = reinterpret_cast<uint32_t*>(S_sc);
-    uint8_t* hop_fr = S_ex;
-    for (uint32_t h = tid; h < nh1; h += nt) {
-        const uint32_t h1 = h < k ? a.L_ids[u * k + h] : a.R_ids[u * k + (h - k)];
-        hop_id[h] = h1;
-        hop_fr[h] = h < k ? a.L_fr[u * k + h] : a.R_fr[u * k + (h - k)];
-        hop_rc[h] = a.R_cnt[h1];
-    }
-    __syncthreads();
-    const uint32_t items = nh1 * (2 * k);
-    constexpr uint32_t kHopU = 4;
-    for (uint32_t it0 = tid; it0 < items; it0 += nt * kHopU) {
-        uint32_t h2[kHopU];
-        uint8_t f2[kHopU];
-        bool ok[kHopU], f1[kHopU];
-#pragma unroll
-        for (uint32_t q = 0; q < kHopU; ++q) {
-            const uint32_t it = min(it0 + q * nt, items - 1);
-            const uint32_t h = it / (2 * k), j = it % (2 * k);
-            const uint64_t h1 = hop_id[h];
-            const bool fwd = j < k;
-            const uint32_t jj = fwd ? j : j - k;
-            ok[q] = it0 + q * nt < items && (fwd || jj < hop_rc[h]);
-            f1[q] = hop_fr[h];
-            // (unconditional loads: jj < k stays inside h1's row)
-            h2[q] = fwd ? a.L_ids[h1 * k + jj] : a.R_ids[h1 * k + jj];
-            f2[q] = fwd ? a.L_fr[h1 * k + jj] : a.R_fr[h1 * k + jj];
-        }
-#pragma unroll
-        for (uint32_t q = 0; q < kHopU; ++q)
-            if (ok[q] && h2[q] != u) pool_insert(keys, fbits, mask, h2[q], f1[q] || f2[q]);
-    }
-    __syncthreads();
-    lap(kKnPhPool);
 
     // Score fresh, new candidates; merge survivors into the running top-k.
     const double unorm = a.c.dnorm[u];
@@ -557,6 +503,77 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     auto certain = [&](double va, uint8_t ea, double vb, uint8_t eb) {
         return (ea && eb) || fabs(va - vb) > 1.25 * ((ea ? 0.0 : eps) + (eb ? 0.0 : eps));
     };
+    // The two-hop pool is built and scored in `nparts` parts: candidate ids
+    // are split by a multiplicative hash, so each part's set fits a pool of
+    // pool_cap slots (<= 16K: two CTAs share an SM and overlap each other's
+    // barrier waits).  The result is the top-k of the union either way.
+    const uint32_t mask = a.pool_cap - 1;
+    auto part_of = [&](uint32_t id) { return a.nparts == 1 ? 0u : (id * 0x9E3779B1u) >> a.pshift; };
+    for (uint32_t part = 0; part < a.nparts; ++part) {
+    for (uint32_t j = tid; j < a.pool_cap; j += nt) keys[j] = kEmpty;
+    for (uint32_t j = tid; j < a.pool_cap / 32; j += nt) {
+        fbits[j] = 0;
+        hbits[j] = 0;
+    }
+    __syncthreads();
+    // L[u] members of this part: mark as "have" (their scores are known;
+    // knn_graph.cpp:122-131 — the snapshot list, not the evolving one)
+    for (uint32_t j = tid; j < k; j += nt) {
+        const uint32_t id = a.L_ids[u * k + j];
+        if (part_of(id) != part) continue;
+        uint32_t s = hslot(id, mask);
+        for (uint32_t probe = 0; probe < a.pool_cap; ++probe) {
+            const uint32_t prev = atomicCAS(&keys[s], kEmpty, id);
+            if (prev == kEmpty || prev == id) break;
+            s = (s + 1) & mask;
+        }
+        atomicOr(&hbits[s >> 5], 1u << (s & 31));
+    }
+    __syncthreads();
+    // Two-hop pool through forward + reverse adjacency (knn_graph.cpp:97-110).
+    // u's first hops (forward list, then reverse list) are staged in shared
+    // memory (the candidate buffers are free until scoring); each thread then
+    // has kHopU second-hop loads in flight before its inserts (the pool is a
+    // set with OR-ed freshness, so insertion order does not matter).
+    const uint32_t rc_u = a.R_cnt[u];
+    const uint32_t nh1 = k + rc_u;
+    uint32_t* hop_id = S_id;
+    uint32_t* hop_rc = reinterpret_cast<uint32_t*>(S_sc);
+    uint8_t* hop_fr = S_ex;
+    for (uint32_t h = tid; h < nh1; h += nt) {
+        const uint32_t h1 = h < k ? a.L_ids[u * k + h] : a.R_ids[u * k + (h - k)];
+        hop_id[h] = h1;
+        hop_fr[h] = h < k ? a.L_fr[u * k + h] : a.R_fr[u * k + (h - k)];
+        hop_rc[h] = a.R_cnt[h1];
+    }
+    __syncthreads();
+    const uint32_t items = nh1 * (2 * k);
+    constexpr uint32_t kHopU = 4;
+    for (uint32_t it0 = tid; it0 < items; it0 += nt * kHopU) {
+        uint32_t h2[kHopU];
+        uint8_t f2[kHopU];
+        bool ok[kHopU], f1[kHopU];
+#pragma unroll
+        for (uint32_t q = 0; q < kHopU; ++q) {
+            const uint32_t it = min(it0 + q * nt, items - 1);
+            const uint32_t h = it / (2 * k), j = it % (2 * k);
+            const uint64_t h1 = hop_id[h];
+            const bool fwd = j < k;
+            const uint32_t jj = fwd ? j : j - k;
+            ok[q] = it0 + q * nt < items && (fwd || jj < hop_rc[h]);
+            f1[q] = hop_fr[h];
+            // (unconditional loads: jj < k stays inside h1's row)
+            h2[q] = fwd ? a.L_ids[h1 * k + jj] : a.R_ids[h1 * k + jj];
+            f2[q] = fwd ? a.L_fr[h1 * k + jj] : a.R_fr[h1 * k + jj];
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kHopU; ++q)
+            if (ok[q] && h2[q] != u && part_of(h2[q]) == part)
+                pool_insert(keys, fbits, mask, h2[q], f1[q] || f2[q], a.pool_cap, a.overflow);
+    }
+    __syncthreads();
+    lap(kKnPhPool);
+
     // compact the candidates (fresh, not already in L[u]) to the front of
     // keys[]: the scoring rounds then cover only real candidates (late passes
     // have ~100 in a 32K-slot table, and every round costs a memory round
@@ -582,7 +599,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
     const uint32_t n_c = n_cand;
     uint32_t round = 0;
     for (uint32_t base = 0; base < n_c; ++round) {
-      const uint32_t end = min(n_c, base + (round == 0 ? 1u : round == 1 ? 2u : uint32_t(kSRounds)) * nt);
+      const uint32_t grow = part > 0 ? uint32_t(kSRounds) : round == 0 ? 1u : round == 1 ? 2u : uint32_t(kSRounds);
+      const uint32_t end = min(n_c, base + grow * nt);
       for (uint32_t b2 = base; b2 < end; b2 += nt) {
         const uint32_t s = b2 + tid;
         const bool cand = s < end;
@@ -623,7 +641,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
                     count(kKnCand, F);
                     count(kKnDense, __popc(km));
                 }
-                const double D = approx::dense_group<NQ4>(a.c, qd, cn, lane, km);
+                const double D = approx::dense_group<NQ4, 2>(a.c, qd, cn, lane, km);
                 const double v = __dadd_rn(__dadd_rn(D, L), S);
                 if (keep && !(v + eps < tau_lo)) {  // may enter: kept with its approximation
                     const uint32_t slot = atomicAdd(&S_cnt, 1u);
@@ -776,6 +794,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) knn_pass_kernel(PassArgs a) {
         __syncthreads();
         lap(kKnPhMerge);
     }
+    }  // parts
+
     // the list's entries that carry approximations get their exact scores
     // (the order among them was certified, so it is the exact order).  Their
     // dense rows are staged in shared memory by the whole CTA (coalesced; the
@@ -816,6 +836,30 @@ size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uin
     return b;
 }
 
+// Pool slots for `items` expected distinct candidates (load factor <= 2/3).
+uint32_t pool_slots(double items) {
+    uint32_t cap = kPassThreads;
+    while (cap < items * 1.5) cap <<= 1;
+    return cap;
+}
+
+// The pool plan of a pass: the worst-case distinct two-hop candidates of a
+// node, min(n, (2k)^2 + k), split into the fewest power-of-two hash parts
+// whose pools let two CTAs share an SM (<= kSmemTwo bytes each, with a 4
+// sigma + 64 margin per part for the hash split; a part that still
+// overflows fails the pass loudly).
+constexpr size_t kSmemTwo = 113 * 1024;
+void pool_plan(uint64_t n, uint32_t k, uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t l_vocab,
+               uint32_t& cap, uint32_t& nparts) {
+    const double worst = static_cast<double>(std::min<uint64_t>(n, 4ull * k * k + k));
+    for (nparts = 1;; nparts <<= 1) {
+        const double per = nparts == 1 ? worst : worst / nparts + 4.0 * std::sqrt(worst / nparts) + 64.0;
+        cap = pool_slots(per);
+        if (pass_smem(dstride, lcap, scap, k, cap, l_vocab) <= kSmemTwo || cap <= kPassThreads || nparts >= 64)
+            return;
+    }
+}
+
 int pass_nq4(uint32_t dstride) {
     const uint32_t need = ((dstride >> 2) + 31) / 32;
     for (int v : {1, 2, 3, 4, 6, 8})
@@ -828,13 +872,6 @@ void launch_pass(const PassArgs& a, uint64_t blocks, size_t sm, cudaStream_t s) 
     FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel<NQ4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     knn_pass_kernel<NQ4><<<(unsigned)blocks, kPassThreads, sm, s>>>(a);
     FGB_LAUNCH("knn_pass_kernel");
-}
-
-uint32_t pool_capacity(uint64_t n, uint32_t k) {
-    const uint64_t worst = std::min<uint64_t>(n, 4ull * k * k + k);
-    uint32_t cap = kPassThreads;
-    while (cap < worst + worst / 2) cap <<= 1;  // load factor <= 2/3 at the worst case
-    return cap;
 }
 
 // Host-side partial Fisher-Yates (knn_graph.cpp:37-46) when 4k >= n.
@@ -945,8 +982,8 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     const uint32_t lcap = hash_capacity(c.max_lnnz), scap = hash_capacity(c.max_snnz);
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
-               next.fresh.get(), d_changed, pool_capacity(g.n, k), lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin};
+               next.fresh.get(), d_changed, 0, lcap, scap, lo,
+               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin, 1, 32, nullptr};
     if (const char* e = std::getenv("FGB_KNN_SORT_MIN")) a.sort_min = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FGB_KNN_PREFETCH")) a.prefetch = std::atoi(e);
     DevBuf<unsigned long long> timing;
@@ -975,7 +1012,23 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     a.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
     a.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
     a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;
-    if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab) > 227 * 1024) a.l_vocab = 0;
+    pool_plan(g.n, k, c.dstride, lcap, scap, a.l_vocab, a.pool_cap, a.nparts);
+    if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab) > 227 * 1024) {
+        a.l_vocab = 0;
+        pool_plan(g.n, k, c.dstride, lcap, scap, 0, a.pool_cap, a.nparts);
+    }
+    if (const char* e = std::getenv("FGB_KNN_PARTS")) {  // dev/test: force a part count (power of two)
+        const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+        if (v >= 1 && (v & (v - 1)) == 0) {
+            a.nparts = v;
+            const double worst = static_cast<double>(std::min<uint64_t>(g.n, 4ull * k * k + k));
+            a.pool_cap = pool_slots(v == 1 ? worst : worst / v + 4.0 * std::sqrt(worst / v) + 64.0);
+        }
+    }
+    a.pshift = 32 - static_cast<uint32_t>(__builtin_ctz(a.nparts));
+    DevBuf<unsigned int> overflow(1);
+    overflow.zero(s);
+    a.overflow = overflow.get();
     const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab);
     if (sm > 227 * 1024)
         throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
@@ -993,6 +1046,12 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         case 8: launch_pass<8>(a, blocks, sm, s); break;
         default: launch_pass<0>(a, blocks, sm, s); break;
     }
+    {
+        unsigned int ov = 0;
+        overflow.download(&ov, 1, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        if (ov) throw Error("internal", "NN-Descent pool overflow (" + std::to_string(ov) + " candidates)");
+    }
     if (a.timing) {
         FGB_CUDA(cudaEventRecord(e1, s));
         unsigned long long t[kKnCount];
@@ -1004,10 +1063,10 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         cudaEventDestroy(e1);
         const double nb = double(blocks);
         std::fprintf(stderr,
-                     "[knn pass] %llu nodes, %.1f ms, smem %zu B, pool_cap %u | cycles/node: init %.0f pool %.0f "
+                     "[knn pass] %llu nodes, %.1f ms, smem %zu B, pool_cap %u x %u parts | cycles/node: init %.0f pool %.0f "
                      "score %.0f merge %.0f exact %.0f final %.0f | per node: cand %.1f dense %.1f enter %.1f rounds %.1f "
                      "resolved %.2f\n",
-                     (unsigned long long)blocks, ms, sm, a.pool_cap, t[kKnPhInit] / nb, t[kKnPhPool] / nb,
+                     (unsigned long long)blocks, ms, sm, a.pool_cap, a.nparts, t[kKnPhInit] / nb, t[kKnPhPool] / nb,
                      t[kKnPhScore] / nb, t[kKnPhMerge] / nb, t[kKnPhExact] / nb, t[kKnPhFinal] / nb, t[kKnCand] / nb, t[kKnDense] / nb,
                      t[kKnEnter] / nb, t[kKnRounds] / nb, t[kKnResolved] / nb);
     }

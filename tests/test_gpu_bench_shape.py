@@ -89,3 +89,15 @@ def test_brute_force_topk_d768(shape, ref):
     assert np.array_equal(g.hit_count, r.hit_count)
     assert np.array_equal(g.doc_id, r.doc_id)
     assert np.array_equal(g.score.view(np.uint64), r.score.view(np.uint64))
+
+
+def test_knn_pass_forced_parts_identical(shape, ref, monkeypatch):
+    """The pass splits the two-hop pool into hash parts (knn.cu pool_plan);
+    eight parts (more than the plan picks at any size) give the same lists."""
+    c, dev, st = shape["c"], shape["dev"], shape["st"]
+    r0 = ref.knn_init(st, c.n, 64, 7, threads=THREADS)
+    r1 = ref.knn_iterate(st, *r0, threads=THREADS)
+    monkeypatch.setenv("FGB_KNN_PARTS", "8")
+    g1 = fg.nn_descent_iterate(dev, *r0)
+    _same_lists(g1, r1, "pass 1, 8 parts")
+    assert g1[3] == r1[3]
