@@ -186,11 +186,11 @@ __device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, ui
     for (int k = 0; k < NQ4; ++k) b[k] = __ldg(row + min(k * 32 + lane, n4 - 1));
 }
 
-// Rows in flight per round trip of dense_group: narrow rows (d <= 256) keep
-// more of them in registers, so a batch of F candidates costs F/kRows
-// dependent round trips instead of F/2.
+// Rows in flight per round trip of dense_group: 4 up to d = 768 (search at
+// configs[1]: 113K -> 120K QPS over 2 rows, B200), 8 for d <= 128, so a batch
+// of F candidates costs F/rows dependent round trips.
 template <int NQ4>
-constexpr int dense_rows() { return NQ4 == 1 ? 8 : (NQ4 == 2 ? 4 : 2); }
+constexpr int dense_rows() { return NQ4 == 1 ? 8 : (NQ4 <= 6 ? 4 : 2); }
 
 // Reduce-scatter of R per-lane partial sums (R a power of two <= 8): row r's
 // total (over all 32 lanes) ends in lanes [r * 32/R, (r + 1) * 32/R).

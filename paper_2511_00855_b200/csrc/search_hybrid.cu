@@ -555,7 +555,8 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
             mark(kHybSparse);
             if (keep && Q.qd && (a.prefetch & 1))
                 l2_prefetch(c.dense + static_cast<uint64_t>(cn) * c.dstride, c.dstride * 4);
-            const double D = Q.qd ? dense_group<NQ4>(c, Q.qd, cn, lane, km) : 0.0;
+            // (2 dense rows per round trip: 4 cost this larger kernel two query-warps per SM)
+            const double D = Q.qd ? dense_group<NQ4, 2>(c, Q.qd, cn, lane, km) : 0.0;
             const uint32_t m = __popc(km);
             mark(kHybDense);
             if (m == 0) continue;
