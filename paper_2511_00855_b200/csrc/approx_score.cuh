@@ -65,6 +65,21 @@ __device__ __forceinline__ float q_lookup(const PathQ& P, uint32_t t, bool& foun
     return P.vocab ? q_lookup_t<true>(P, t, found) : q_lookup_t<false>(P, t, found);
 }
 
+// Lookup modes of a search kernel instantiation: every active sparse path of
+// the batch uses the hash (0) or the bitmap (1), or each path its own (2).
+// One mode per instantiation keeps a single lookup variant in the hot loop
+// (instruction-cache footprint).
+enum : int { kModeHash = 0, kModeBitmap = 1, kModeMixed = 2 };
+template <int kMode>
+__device__ __forceinline__ float q_lookup_m(const PathQ& P, uint32_t t, bool& found) {
+    if constexpr (kMode == kModeBitmap)
+        return q_lookup_t<true>(P, t, found);
+    else if constexpr (kMode == kModeHash)
+        return q_lookup_t<false>(P, t, found);
+    else
+        return q_lookup(P, t, found);
+}
+
 // ------------------------------------------------------------ scoring
 // The query terms among 4 postings.  kF32 = false: exact fp64 products summed
 // in fp64 (each product predicated on the lookup hit).  kF32 = true: fp32

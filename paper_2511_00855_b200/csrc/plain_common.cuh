@@ -62,6 +62,7 @@ struct QueryQ {
 // dense rows and the (kPad, 0) padding of posting groups add nothing.
 // (Kept inline: an out-of-line call here corrupted live batch registers
 // under sm_100a ptxas 12.9 — tools/smoke_plain.py reproduced it.)
+template <int kMode = approx::kModeMixed>
 __device__ __forceinline__ double exact_dist(const DevCorpus& c, const QueryQ& Q, uint32_t node) {
     double acc = 0.0;
     if (Q.qd) {
@@ -127,7 +128,7 @@ __device__ __forceinline__ double exact_dist(const DevCorpus& c, const QueryQ& Q
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         bool f;
-                        const float q = q_lookup(P, t[e], f);
+                        const float q = approx::q_lookup_m<kMode>(P, t[e], f);
                         if (f) s = __fma_rn((double)q, (double)v[e], s);
                     }
                 }

@@ -78,7 +78,7 @@ __device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch
     return m;
 }
 
-template <int NQ4, bool kTime>
+template <int NQ4, bool kTime, int kMode>
 __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t lane = threadIdx.x & 31;
@@ -246,8 +246,14 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                 const uint32_t* pidx = learned ? c.l_idx : c.s_idx;
                 const float* pval = learned ? c.l_val : c.s_val;
                 const uint32_t off4 = learned ? mt.x : mt.y, pnnz = learned ? (mt.z & 0xFFFFu) : (mt.z >> 16);
-                const double r = P.vocab ? sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F)
-                                         : sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
+                double r;
+                if constexpr (kMode == approx::kModeBitmap)
+                    r = sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F);
+                else if constexpr (kMode == approx::kModeHash)
+                    r = sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
+                else
+                    r = P.vocab ? sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F)
+                                : sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
                 if (learned)
                     L = r;
                 else
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                 const uint32_t fxm = __ballot_sync(kFull, fix);
                 if (!fxm && !ntm && !ncm) break;
                 if (fix) {
-                    d = exact_dist(c, Q, n & kId);
+                    d = exact_dist<kMode>(c, Q, n & kId);
                     n |= kExact;
                 }
                 resolved += __popc(fxm);
@@ -346,7 +352,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                         const int i = static_cast<int>(__shfl_sync(kFull, rk, j)) - 4 + static_cast<int>(lane);
                         const bool pf = lane < 8 && i >= 0 && i < static_cast<int>(sz) && !(P.n[i] & kExact);
                         if (pf) {
-                            P.d[i] = exact_dist(c, Q, P.n[i] & kId);
+                            P.d[i] = exact_dist<kMode>(c, Q, P.n[i] & kId);
                             P.n[i] |= kExact;
                         }
                         resolved += __popc(__ballot_sync(kFull, pf));
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
         // (keyword_postfilter with no required keywords: topk as is, search.cpp:100-139)
         for (uint32_t i = lane; i < tsize; i += 32) {
             if (!(w.topk_n[i] & kExact)) {
-                w.topk_d[i] = exact_dist(c, Q, w.topk_n[i] & kId);
+                w.topk_d[i] = exact_dist<kMode>(c, Q, w.topk_n[i] & kId);
                 ++final_exact;
             }
             a.r_node[static_cast<uint64_t>(qi) * a.hit_stride + i] = w.topk_n[i] & kId;
@@ -408,18 +414,27 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
     }
 }
 
-template <int NQ4>
-void launch_t(const PlainLaunch& a, uint64_t blocks, size_t smem, cudaStream_t s) {
+// (the phase-timing variant exists in the mixed mode only)
+template <int NQ4, int kMode>
+void launch_m(const PlainLaunch& a, uint64_t blocks, size_t smem, cudaStream_t s) {
     if (a.timing) {
-        FGB_CUDA(cudaFuncSetAttribute(search_plain_kernel<NQ4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        search_plain_kernel<NQ4, true><<<(unsigned)blocks, 32, smem, s>>>(a);
+        FGB_CUDA(cudaFuncSetAttribute(search_plain_kernel<NQ4, true, approx::kModeMixed>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        search_plain_kernel<NQ4, true, approx::kModeMixed><<<(unsigned)blocks, 32, smem, s>>>(a);
     } else {
-        FGB_CUDA(cudaFuncSetAttribute(search_plain_kernel<NQ4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FGB_CUDA(cudaFuncSetAttribute(search_plain_kernel<NQ4, false, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-        search_plain_kernel<NQ4, false><<<(unsigned)blocks, 32, smem, s>>>(a);
+        search_plain_kernel<NQ4, false, kMode><<<(unsigned)blocks, 32, smem, s>>>(a);
     }
     FGB_LAUNCH("search_plain_kernel");
+}
+
+template <int NQ4>
+void launch_t(const PlainLaunch& a, uint64_t blocks, size_t smem, cudaStream_t s) {
+    switch (a.mode) {
+        case approx::kModeHash: launch_m<NQ4, approx::kModeHash>(a, blocks, smem, s); break;
+        default: launch_m<NQ4, approx::kModeMixed>(a, blocks, smem, s); break;
+    }
 }
 
 int nq4_of(const PlainLaunch& a) {
@@ -430,18 +445,21 @@ int nq4_of(const PlainLaunch& a) {
 }
 
 template <int NQ4>
-const void* kernel_ptr() {
-    return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false>);
+const void* kernel_ptr(int mode) {
+    switch (mode) {
+        case approx::kModeHash: return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false, approx::kModeHash>);
+        default: return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false, approx::kModeMixed>);
+    }
 }
 
-const void* kernel_for(int v) {
+const void* kernel_for(int v, int mode) {
     switch (v) {
-        case 1: return kernel_ptr<1>();
-        case 2: return kernel_ptr<2>();
-        case 3: return kernel_ptr<3>();
-        case 4: return kernel_ptr<4>();
-        case 6: return kernel_ptr<6>();
-        case 8: return kernel_ptr<8>();
+        case 1: return kernel_ptr<1>(mode);
+        case 2: return kernel_ptr<2>(mode);
+        case 3: return kernel_ptr<3>(mode);
+        case 4: return kernel_ptr<4>(mode);
+        case 6: return kernel_ptr<6>(mode);
+        case 8: return kernel_ptr<8>(mode);
         default: return nullptr;
     }
 }
@@ -458,7 +476,7 @@ size_t plain_warp_smem(const PlainLaunch& a) {
 
 uint64_t plain_slots(const PlainLaunch& a, uint64_t nq, int device) {
     const size_t smem = plain_warp_smem(a);
-    const void* k = kernel_for(nq4_of(a));
+    const void* k = kernel_for(nq4_of(a), a.mode);
     FGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, sms = 0;
     FGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem));

@@ -17,6 +17,7 @@ struct PlainLaunch {
     uint32_t entry_count;
     const uint8_t* qflags;      // QF_VALID | QF_FALLBACK
     uint32_t vocab[2];          // per sparse path (learned, statistical): bitmap width, 0 = hash
+    int mode;                   // lookup mode of the batch's active paths (approx::kMode*)
     uint32_t cap[2];            // per sparse path: hash capacity / staged value slots
     uint32_t beamcap, kcap;     // max beam / k in the batch
     double max_norm;            // >= sqrt(max sqnorm) of the corpus

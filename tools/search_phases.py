@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--docs", type=int, default=1_000_000)
 ap.add_argument("--queries", type=int, default=10_000)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--no-timing", action="store_true")
 a = ap.parse_args()
 p = bench.synth_params(a.docs)
 c, kg, _ = synth.generate_corpus(p, 0)
@@ -32,14 +33,16 @@ for _ in range(a.reps):
     fg.batch_query(ix, q, entry_count=entry)
     ms.append(ix.last_search_stats()[0])
 print(f"{ix.last_search_kernel()} {q.count / (min(ms) / 1e3):.1f} QPS (best of {a.reps}: {min(ms):.2f} ms)", flush=True)
-for pf in os.environ.get("PF_SWEEP", "").split():
-    os.environ["FGB_SEARCH_PREFETCH"] = pf
+for pf in os.environ.get("ENV_SWEEP", "").split():  # NAME=VALUE settings, one measurement each
+    name, val = pf.split("=")
+    os.environ[name] = val
     ms = []
     for _ in range(a.reps):
         bench.flush_l2(0)
         fg.batch_query(ix, q, entry_count=entry)
         ms.append(ix.last_search_stats()[0])
-    print(f"  prefetch={pf}: {q.count / (min(ms) / 1e3):.1f} QPS", flush=True)
-os.environ.pop("FGB_SEARCH_PREFETCH", None)
-os.environ["FGB_SEARCH_TIMING"] = "1"
-fg.batch_query(ix, q, entry_count=entry)
+    print(f"  {pf}: {q.count / (min(ms) / 1e3):.1f} QPS", flush=True)
+    del os.environ[name]
+if not a.no_timing:
+    os.environ["FGB_SEARCH_TIMING"] = "1"
+    fg.batch_query(ix, q, entry_count=entry)
