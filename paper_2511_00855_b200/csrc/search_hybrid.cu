@@ -157,9 +157,10 @@ __device__ __forceinline__ int ctx_claim(uint4* t, uint32_t cap, uint32_t node, 
 // CALL, and with calls in this kernel ptxas 12.9 (sm_100a) clobbered live
 // registers (pool sizes and batch nodes, caught by the acceptance suite's
 // criterion 5).
+template <int kMode>
 __device__ __forceinline__ double exact_adj(const DevCorpus& c, const QueryQ& Q, uint32_t node, const uint4* ctx,
                                             uint32_t ctxcap, const double* rew) {
-    double d = exact_dist(c, Q, node);
+    double d = exact_dist<kMode>(c, Q, node);
     if (ctx) {
         const uint4 e = ctx_get(ctx, ctxcap, node);
         if (e.x == node && e.w && e.z >= 1) d = __dsub_rn(d, rew[e.z - 1]);
@@ -224,7 +225,7 @@ __device__ __forceinline__ uint32_t pool_erase(double* pd, uint32_t* pn, uint32_
     return wpos;
 }
 
-template <int NQ4>
+template <int NQ4, int kMode>
 __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaunch h) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const PlainLaunch& a = h.p;
@@ -535,8 +536,12 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
                 const uint32_t* pidx = learned ? c.l_idx : c.s_idx;
                 const float* pval = learned ? c.l_val : c.s_val;
                 const uint32_t off4 = learned ? mt.x : mt.y, pnnz = learned ? (mt.z & 0xFFFFu) : (mt.z >> 16);
-                const double r = P.vocab ? sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F)
-                                         : sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
+                double r;
+                if constexpr (kMode == approx::kModeHash)
+                    r = sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
+                else
+                    r = P.vocab ? sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F)
+                                : sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
                 if (learned)
                     Ls = r;
                 else
@@ -635,7 +640,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
                     nreq += __popc(pm);
                 }
                 __syncwarp();
-                for (uint32_t r = lane; r < nreq; r += 32) w.xd[r] = exact_adj(c, Q, w.xn[r], ctxq, h.ctxcap, rtab);
+                for (uint32_t r = lane; r < nreq; r += 32) w.xd[r] = exact_adj<kMode>(c, Q, w.xn[r], ctxq, h.ctxcap, rtab);
                 __syncwarp();
                 if (fix) {
                     d = w.xd[__popc(fxm & lt)];
@@ -749,7 +754,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
             out = tsize;
         } else if (err == 0) {
             // twin entries at their final adjusted distance, exactly
-            for (uint32_t i = lane; i < ntwin; i += 32) twin_d[i] = exact_adj(c, Q, twin_node[i], ctxq, h.ctxcap, rtab);
+            for (uint32_t i = lane; i < ntwin; i += 32) twin_d[i] = exact_adj<kMode>(c, Q, twin_node[i], ctxq, h.ctxcap, rtab);
             __syncwarp();
             const uint32_t total = tsize + ntwin;
             while (out < K) {
@@ -845,18 +850,19 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
 }
 
 template <int NQ4>
-const void* kernel_ptr() {
-    return reinterpret_cast<const void*>(search_hybrid_kernel<NQ4>);
+const void* kernel_ptr(int mode) {
+    return mode == approx::kModeHash ? reinterpret_cast<const void*>(search_hybrid_kernel<NQ4, approx::kModeHash>)
+                                     : reinterpret_cast<const void*>(search_hybrid_kernel<NQ4, approx::kModeMixed>);
 }
 
-const void* kernel_for(int v) {
+const void* kernel_for(int v, int mode) {
     switch (v) {
-        case 1: return kernel_ptr<1>();
-        case 2: return kernel_ptr<2>();
-        case 3: return kernel_ptr<3>();
-        case 4: return kernel_ptr<4>();
-        case 6: return kernel_ptr<6>();
-        case 8: return kernel_ptr<8>();
+        case 1: return kernel_ptr<1>(mode);
+        case 2: return kernel_ptr<2>(mode);
+        case 3: return kernel_ptr<3>(mode);
+        case 4: return kernel_ptr<4>(mode);
+        case 6: return kernel_ptr<6>(mode);
+        case 8: return kernel_ptr<8>(mode);
         default: return nullptr;
     }
 }
@@ -878,7 +884,7 @@ size_t hybrid_warp_smem(const HybridLaunch& h) {
 
 uint64_t hybrid_slots(const HybridLaunch& h, uint64_t nq, int device) {
     const size_t smem = hybrid_warp_smem(h);
-    const void* k = kernel_for(nq4_of(h.p.c.dstride));
+    const void* k = kernel_for(nq4_of(h.p.c.dstride), h.p.mode);
     FGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0, sms = 0;
     FGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem));
@@ -894,9 +900,15 @@ void launch_search_hybrid(const HybridLaunch& h, uint64_t blocks, cudaStream_t s
     switch (nq4_of(h.p.c.dstride)) {
 #define FGB_HYB(V)                                                                                               \
     case V:                                                                                                      \
-        FGB_CUDA(cudaFuncSetAttribute(search_hybrid_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                      (int)smem));                                                               \
-        search_hybrid_kernel<V><<<(unsigned)blocks, 32, smem, s>>>(h);                                           \
+        if (h.p.mode == approx::kModeHash) {                                                                     \
+            FGB_CUDA(cudaFuncSetAttribute(search_hybrid_kernel<V, approx::kModeHash>,                            \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));              \
+            search_hybrid_kernel<V, approx::kModeHash><<<(unsigned)blocks, 32, smem, s>>>(h);                    \
+        } else {                                                                                                 \
+            FGB_CUDA(cudaFuncSetAttribute(search_hybrid_kernel<V, approx::kModeMixed>,                           \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));              \
+            search_hybrid_kernel<V, approx::kModeMixed><<<(unsigned)blocks, 32, smem, s>>>(h);                   \
+        }                                                                                                        \
         break;
         FGB_HYB(1)
         FGB_HYB(2)
