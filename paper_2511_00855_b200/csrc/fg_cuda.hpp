@@ -230,6 +230,7 @@ struct SearchWorkspace {
     DevBuf<uint32_t> bits;
     DevBuf<uint32_t> lists;
     DevBuf<unsigned char> misc;
+    DevBuf<unsigned char> gpool;  // cand pools in HBM for very large beams
 };
 
 inline uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }

@@ -1022,6 +1022,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) search_kernel(SearchArgs 
 namespace fgb {
 namespace {
 constexpr uint64_t kId30 = 0x3FFFFFFFull;  // node ids must fit 30 bits in the plain kernel's pools
+constexpr uint32_t kGpoolBeam = 1536;       // beams above this keep the plain kernel's cand pool in HBM (B200, 1M docs: beam 1024 smem 45.9K vs HBM 43.0K QPS; 2048: 19.9K vs 20.5K; 3008: 10.3K vs 13.1K)
 
 // Device results -> the caller's fg_search_results (ids -> doc ids, per-query
 // validation errors, counters); records the kernel time of ev0..ev1.
@@ -1451,8 +1452,23 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             if (special) {
                 if (run_hybrid(ix, c, W, pl, q, qflags, max_seeds, max_req, any_ctx, any_req, conj, nq, stride, errs, out, s))
                     return;
-            } else if (plain_warp_smem(pl) > 0) {
+            } else {
+              // very large beams keep their cand pools in HBM (L1/L2 cached):
+              // in shared memory they would cut the query-warps per SM
+              // (FGB_SEARCH_GPOOL=0/1 forces the choice)
+              bool gpool = pl.beamcap > kGpoolBeam;
+              if (const char* e = std::getenv("FGB_SEARCH_GPOOL")) gpool = e[0] == '1';
+              if (gpool) {
+                  pl.gpool_d = reinterpret_cast<double*>(1);  // (placeholders: smem sizing only)
+                  pl.gpool_n = reinterpret_cast<uint32_t*>(1);
+              }
+              if (plain_warp_smem(pl) > 0) {
                 const uint64_t slots = plain_slots(pl, nq, c.device);
+                if (gpool) {
+                    W.gpool.ensure(slots * pl.beamcap * 12);
+                    pl.gpool_d = reinterpret_cast<double*>(W.gpool.get());
+                    pl.gpool_n = reinterpret_cast<uint32_t*>(W.gpool.get() + slots * pl.beamcap * 8);
+                }
                 pl.nwords = (n + 31) / 32;
                 // touched-list capacity: a query visits at most n nodes
                 pl.tcap = 1024;
@@ -1521,6 +1537,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                 ix->last_launches = 1;
                 ix->last_kernel = "search_plain_kernel";
                 return;
+              }
             }
         }
 

@@ -59,7 +59,7 @@ struct PlainMem {
     uint32_t* br;
 };
 
-__device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch& a) {
+__device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch& a, uint64_t slot) {
     PlainMem m;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -70,9 +70,9 @@ __device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch
     m.qd = reinterpret_cast<float*>(take(a.c.dstride * 4));
     m.path[0] = take(path_bytes(a.vocab[0], a.cap[0]));
     m.path[1] = take(path_bytes(a.vocab[1], a.cap[1]));
-    m.cand_d = reinterpret_cast<double*>(take(a.beamcap * 8));
+    m.cand_d = a.gpool_d ? a.gpool_d + slot * a.beamcap : reinterpret_cast<double*>(take(a.beamcap * 8));
     m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
-    m.cand_n = reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
+    m.cand_n = a.gpool_n ? a.gpool_n + slot * a.beamcap : reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
     m.topk_n = reinterpret_cast<uint32_t*>(take(a.kcap * 4));
     m.br = reinterpret_cast<uint32_t*>(take(32 * 4));
     return m;
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t slot = blockIdx.x;
-    PlainMem w = carve(smem_raw, a);
+    PlainMem w = carve(smem_raw, a, slot);
     uint32_t* visited = a.visited + slot * a.nwords;
     uint32_t* touched = a.touched + slot * a.tcap;
     const DevCorpus& c = a.c;
@@ -469,8 +469,8 @@ const void* kernel_for(int v, int mode) {
 size_t plain_warp_smem(const PlainLaunch& a) {
     if (nq4_of(a) == 0) return 0;  // dense rows wider than 1,024 floats: general kernel
     const size_t b = al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0])) +
-                     al16(path_bytes(a.vocab[1], a.cap[1])) + al16(a.beamcap * 8) + al16(a.kcap * 8) +
-                     al16(a.beamcap * 4) + al16(a.kcap * 4) + al16(32 * 4);
+                     al16(path_bytes(a.vocab[1], a.cap[1])) + (a.gpool_d ? 0 : al16(a.beamcap * 8)) + al16(a.kcap * 8) +
+                     (a.gpool_n ? 0 : al16(a.beamcap * 4)) + al16(a.kcap * 4) + al16(32 * 4);
     return b <= 227 * 1024 ? b : 0;
 }
 

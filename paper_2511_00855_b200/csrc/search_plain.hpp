@@ -20,6 +20,8 @@ struct PlainLaunch {
     int mode;                   // lookup mode of the batch's active paths (approx::kMode*)
     uint32_t cap[2];            // per sparse path: hash capacity / staged value slots
     uint32_t beamcap, kcap;     // max beam / k in the batch
+    double* gpool_d;            // non-null: the cand pools live in HBM (beamcap per query-warp), not smem
+    uint32_t* gpool_n;
     double max_norm;            // >= sqrt(max sqnorm) of the corpus
     double max_dnorm;           // >= max dense-row norm of the corpus
     double eps_coef;            // fp64 error-bound coefficient (see search_plain.cu)

@@ -156,3 +156,14 @@ def test_plain_buffer_reuse_and_pinned_inputs(c2_small, ref):
     same(g, ref.batch_query(rix, bad, entry_count=32, threads=thr))
     assert g.error(1).startswith("invalid-k") and g.hit_count[1] == 0
     same(fg.batch_query(gix, big.pinned(), entry_count=32), ref.batch_query(rix, big, entry_count=32, threads=thr))
+
+
+def test_plain_hbm_cand_pool_identical(c2_small, ref, monkeypatch):
+    """Beams above kGpoolBeam keep the cand pool in HBM instead of shared
+    memory (search.cu); forced on here at small beams, results unchanged."""
+    monkeypatch.setenv("FGB_SEARCH_GPOOL", "1")
+    p, c, dc, gix, rix = c2_small
+    for beam in (96, 2100):  # (2100: above the threshold without the override)
+        q = synth.synth_queries(p, 32, beam_width=beam)
+        same(fg.batch_query(gix, q, entry_count=64), ref.batch_query(rix, q, entry_count=64))
+        assert gix.last_search_kernel() == "search_plain_kernel"

@@ -19,12 +19,15 @@ ap.add_argument("--docs", type=int, default=1_000_000)
 ap.add_argument("--queries", type=int, default=10_000)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--no-timing", action="store_true")
+ap.add_argument("--beam", type=int, default=0)
+ap.add_argument("--entry", type=int, default=0)
 a = ap.parse_args()
 p = bench.synth_params(a.docs)
 c, kg, _ = synth.generate_corpus(p, 0)
 dc = fg.DeviceCorpus(c)
 ix = fg.build_hybrid_index(dc, kg, **bench.BUILD)
-entry, beam = bench.OPERATING_POINT["entry"], bench.OPERATING_POINT["beam"]
+entry = a.entry or bench.OPERATING_POINT["entry"]
+beam = a.beam or bench.OPERATING_POINT["beam"]
 q = bench.c2_queries(p, a.queries, bench.TIMED_STREAM).with_(beam_width=beam)
 fg.batch_query(ix, q, entry_count=entry)
 ms = []
