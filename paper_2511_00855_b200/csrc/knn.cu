@@ -137,6 +137,7 @@ struct PassArgs {
     uint32_t nparts;    // the two-hop pool is processed in nparts hash parts (power of two)
     uint32_t pshift;    // part of id = (id * 0x9E3779B1) >> pshift
     unsigned int* overflow;  // pool overflow counter (0 after a correct pass)
+    const uint32_t* order;   // CTA b processes node order[lo + b] (graph locality); nullptr: lo + b
 };
 
 enum : int {
@@ -398,7 +399,7 @@ template <int NQ4>
 __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
-    const uint64_t u = a.lo + blockIdx.x;
+    const uint64_t u = a.order ? a.order[a.lo + blockIdx.x] : a.lo + blockIdx.x;
     const uint32_t tid = threadIdx.x, nt = blockDim.x;
     SmemQuery sq;
     unsigned char* p = smem + ((doc_stage_bytes(a.c.dstride, a.lcap, a.scap) + 15) & ~size_t(15));
@@ -983,7 +984,9 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, 0, lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin, 1, 32, nullptr};
+               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin, 1, 32, nullptr, nullptr};
+    // (results do not depend on the order nodes are processed in)
+    if (R.order.size() == g.n && lo == 0 && hi == g.n) a.order = R.order.get();
     if (const char* e = std::getenv("FGB_KNN_SORT_MIN")) a.sort_min = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FGB_KNN_PREFETCH")) a.prefetch = std::atoi(e);
     DevBuf<unsigned long long> timing;
@@ -1095,6 +1098,37 @@ uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
     return knn_iterate_device(c, g, s, R, next, changed);
 }
 
+// BFS order over the first kOrderNbrs entries of every forward list (a
+// permutation of [0, n)), uploaded to `order`.
+constexpr uint64_t kOrderMinNodes = 65536;
+constexpr uint32_t kOrderNbrs = 16;
+void locality_order(const DevKnn& g, DevBuf<uint32_t>& order, cudaStream_t s) {
+    const uint64_t n = g.n;
+    const uint32_t k = g.k, w = std::min(k, kOrderNbrs);
+    std::vector<uint32_t> ids(n * k);
+    g.ids.download(ids.data(), ids.size(), s);
+    FGB_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> ord;
+    ord.reserve(n);
+    std::vector<uint8_t> seen(n, 0);
+    for (uint64_t root = 0; root < n; ++root) {
+        if (seen[root]) continue;
+        seen[root] = 1;
+        uint64_t head = ord.size();
+        ord.push_back(static_cast<uint32_t>(root));
+        while (head < ord.size()) {
+            const uint64_t u = ord[head++];
+            const uint32_t* l = ids.data() + u * k;
+            for (uint32_t j = 0; j < w; ++j)
+                if (!seen[l[j]]) {
+                    seen[l[j]] = 1;
+                    ord.push_back(l[j]);
+                }
+        }
+    }
+    order.upload(ord, s);
+}
+
 uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
                           double convergence, uint64_t seed, DevKnn& g, cudaStream_t s) {
     uint32_t k = k_req;
@@ -1112,6 +1146,14 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
         ht.mark("pass");
         ++passes;
         if (static_cast<double>(changed) / denom < convergence) break;
+        // After pass 1 the lists are neighbourhoods: later passes visit the
+        // nodes in BFS order over them, so the CTAs resident at one time work
+        // on overlapping two-hop pools and their candidate rows meet in L2.
+        const char* oe = std::getenv("FGB_KNN_ORDER");
+        if (it == 0 && c.n >= kOrderMinNodes && !(oe && oe[0] == '0')) {
+            locality_order(g, R.order, s);
+            ht.mark("order");
+        }
     }
     return passes;
 }

@@ -31,6 +31,9 @@ struct ReverseLists {
     DevBuf<uint64_t> keys_a, keys_b;
     DevBuf<uint32_t> vals_a, vals_b, tkeys_a, tkeys_b, tcnt, tstart;
     DevBuf<unsigned char> temp;
+    // node visiting order of the pass kernel (graph locality, set after
+    // pass 1 by knn_build_device; empty: identity)
+    DevBuf<uint32_t> order;
 };
 
 // init_random_graph (knn_graph.cpp:52-73) into g (allocated n x k).
