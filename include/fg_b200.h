@@ -350,6 +350,18 @@ int fg_comm_unique_id(uint8_t* id /* FG_COMM_ID_BYTES */);
 int fg_comm_init(int nranks, int rank, const uint8_t* id, int device, fg_comm** out);
 int fg_comm_free(fg_comm* comm);
 
+/* A communicator whose collectives run through caller callbacks on host
+ * buffers (e.g. torch.distributed gloo) instead of NCCL: the same sharded
+ * build, each collective staged device -> host -> callback -> device.  For
+ * hosts without NCCL peers and for multi-process tests of the sharding with
+ * several ranks on one GPU.  all_gather: `send` holds this rank's `bytes`,
+ * `recv` receives every rank's in rank order (nranks * bytes); sum_u64: `x`
+ * (`count` values) is replaced by the sum over ranks.  Return 0 on success. */
+typedef int (*fg_host_all_gather_fn)(void* ctx, const void* send, void* recv, uint64_t bytes);
+typedef int (*fg_host_sum_u64_fn)(void* ctx, uint64_t* x, uint64_t count);
+int fg_comm_init_host(int nranks, int rank, int device, fg_host_all_gather_fn all_gather,
+                      fg_host_sum_u64_fn sum_u64, void* ctx, fg_comm** out);
+
 /* build_hybrid_index (index.hpp:60-61) sharded by vertex range: rank r runs
  * the NN-Descent passes and the per-node refinery for nodes
  * [r*ceil(n/G), (r+1)*ceil(n/G)), all-gathering each pass's lists and the

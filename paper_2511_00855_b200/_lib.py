@@ -70,6 +70,8 @@ def _declare(lib):
         "fg_comm_unique_id": (C.c_int, [A.u8p]),
         "fg_comm_init": (C.c_int, [C.c_int, C.c_int, A.u8p, C.c_int, P(C.c_void_p)]),
         "fg_comm_free": (C.c_int, [C.c_void_p]),
+        "fg_comm_init_host": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        P(C.c_void_p)]),
         "fg_index_build_sharded": (C.c_int, [C.c_void_p, P(A.KgView), P(A.BuildParams), C.c_void_p,
                                              C.c_uint32, P(C.c_void_p)]),
         "fg_index_free": (C.c_int, [C.c_void_p]),

@@ -49,7 +49,7 @@ const NcclApi& nccl() {
     static NcclApi api = [] {
         NcclApi a;
         for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-            a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            a.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);  // (GLOBAL would shadow the NCCL torch loads later)
             if (a.h) break;
         }
         if (!a.h) return a;
@@ -80,6 +80,10 @@ double secs(Clock::time_point a) { return std::chrono::duration<double>(Clock::n
 struct fg_comm {
     int rank = 0, size = 1, device = 0;
     ncclComm_t comm = nullptr;
+    // host transport (fg_comm_init_host): collectives through callbacks
+    fg_host_all_gather_fn host_gather = nullptr;
+    fg_host_sum_u64_fn host_sum = nullptr;
+    void* host_ctx = nullptr;
 };
 
 namespace fgb {
@@ -101,11 +105,30 @@ struct Shards {
         if (!comm || G == 1) return;
         const size_t count = cn * row_elems * sizeof(T);
         unsigned char* base = reinterpret_cast<unsigned char*>(buf.get());
+        if (comm->host_gather) {  // device -> host -> callback -> device
+            std::vector<unsigned char> mine(count), all(count * G);
+            FGB_CUDA(cudaMemcpyAsync(mine.data(), base + comm->rank * count, count, cudaMemcpyDeviceToHost, s));
+            FGB_CUDA(cudaStreamSynchronize(s));
+            if (comm->host_gather(comm->host_ctx, mine.data(), all.data(), count) != 0)
+                throw Error("comm-error", "host all-gather callback failed");
+            FGB_CUDA(cudaMemcpyAsync(base, all.data(), all.size(), cudaMemcpyHostToDevice, s));
+            FGB_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
         nccl_check(nccl().allGather(base + comm->rank * count, base, count, ncclUint8, comm->comm, s),
                    "ncclAllGather");
     }
     void sum(DevBuf<unsigned long long>& x, cudaStream_t s) const {
         if (!comm || G == 1) return;
+        if (comm->host_sum) {
+            uint64_t v = 0;
+            FGB_CUDA(cudaMemcpyAsync(&v, x.get(), 8, cudaMemcpyDeviceToHost, s));
+            FGB_CUDA(cudaStreamSynchronize(s));
+            if (comm->host_sum(comm->host_ctx, &v, 1) != 0) throw Error("comm-error", "host sum callback failed");
+            FGB_CUDA(cudaMemcpyAsync(x.get(), &v, 8, cudaMemcpyHostToDevice, s));
+            FGB_CUDA(cudaStreamSynchronize(s));
+            return;
+        }
         nccl_check(nccl().allReduce(x.get(), x.get(), 1, ncclUint64, ncclSum, comm->comm, s), "ncclAllReduce");
     }
 };
@@ -218,6 +241,23 @@ int fg_comm_init(int nranks, int rank, const uint8_t* id, int device, fg_comm** 
         ncclUniqueId uid;
         std::memcpy(uid.internal, id, sizeof(uid.internal));
         nccl_check(nccl().commInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+        *out = c.release();
+    });
+}
+
+int fg_comm_init_host(int nranks, int rank, int device, fg_host_all_gather_fn all_gather, fg_host_sum_u64_fn sum_u64,
+                      void* ctx, fg_comm** out) {
+    return guarded([&] {
+        if (!all_gather || !sum_u64 || !out) throw Error("invalid-argument", "null pointer");
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw Error("invalid-argument", "bad rank / size");
+        require_device(device);
+        auto c = std::make_unique<fg_comm>();
+        c->rank = rank;
+        c->size = nranks;
+        c->device = device;
+        c->host_gather = all_gather;
+        c->host_sum = sum_u64;
+        c->host_ctx = ctx;
         *out = c.release();
     });
 }

@@ -256,12 +256,21 @@ class Comm:
     ID_BYTES = 128
 
     @staticmethod
+    def _torch_nccl_first():
+        """The library dlopens libnccl.so.2 on first use; in a PyTorch process
+        that must resolve to the NCCL torch bundles (once a libnccl.so.2 is
+        loaded, torch's own can no longer be)."""
+        import torch  # noqa: F401  (loads torch's libnccl)
+
+    @staticmethod
     def unique_id() -> bytes:
+        Comm._torch_nccl_first()
         buf = np.zeros(Comm.ID_BYTES, np.uint8)
         check(lib().fg_comm_unique_id(A.ptr(buf, A.u8p)))
         return buf.tobytes()
 
     def __init__(self, nranks: int, rank: int, uid: bytes, device: int = 0):
+        Comm._torch_nccl_first()
         buf = np.frombuffer(uid, np.uint8).copy()
         h = C.c_void_p()
         check(lib().fg_comm_init(nranks, rank, A.ptr(buf, A.u8p), device, C.byref(h)))
@@ -277,6 +286,48 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+_HOST_GATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+_HOST_SUM = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64)
+
+
+class HostComm(Comm):
+    """A sharded-build communicator whose collectives run on host buffers
+    through torch.distributed (fg_comm_init_host) — any backend, e.g. gloo.
+    Lets several ranks share one GPU (NCCL refuses that), so the multi-rank
+    build is exercised by multi-process tests on a single-GPU box."""
+
+    def __init__(self, nranks: int, rank: int, device: int = 0):
+        import torch
+        import torch.distributed as dist
+
+        def gather(_ctx, send, recv, nbytes):
+            try:
+                src = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send)).copy()
+                parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(nranks)]
+                dist.all_gather(parts, torch.from_numpy(src))
+                dst = np.ctypeslib.as_array((C.c_uint8 * (nbytes * nranks)).from_address(recv))
+                dst[:] = torch.cat(parts).numpy()
+                return 0
+            except Exception:  # reported to the library as a failed collective
+                return 1
+
+        def total(_ctx, x, count):
+            try:
+                t = torch.tensor([int(x[i]) for i in range(count)], dtype=torch.int64)
+                dist.all_reduce(t)
+                for i in range(count):
+                    x[i] = int(t[i])
+                return 0
+            except Exception:
+                return 1
+
+        self._cb = (_HOST_GATHER(gather), _HOST_SUM(total))  # kept alive with the comm
+        h = C.c_void_p()
+        check(lib().fg_comm_init_host(nranks, rank, device, C.cast(self._cb[0], C.c_void_p),
+                                      C.cast(self._cb[1], C.c_void_p), None, C.byref(h)))
+        self.h, self.rank, self.size = h, rank, nranks
 
 
 def build_hybrid_index_sharded(dc: DeviceCorpus, kg: A.KG | None = None, comm: Comm | None = None,

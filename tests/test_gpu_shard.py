@@ -56,3 +56,52 @@ def test_single_rank_communicator(corpus3k):
     got = fg.build_hybrid_index_sharded(dc, kg, comm=comm, **BUILD).export()
     comm.close()
     same_index(got, fg.build_hybrid_index(dc, kg, **BUILD).export())
+
+
+# ------------------------------------------------ real ranks, one GPU
+def _free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def _shard_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = A.synth_params(docs=3001, dense_dim=64, learned_vocab=5000, learned_nnz=24,
+                           statistical_vocab=5000, statistical_nnz=16, entity_vocab=400,
+                           kg_triplets=1500, chains=10, answers_per_chain=4, seed=13)
+        c, kg, _ = synth.generate_corpus(p, 0)
+        dc = fg.DeviceCorpus(c, device=0)
+        comm = fg.HostComm(world, rank, 0)
+        ix = fg.build_hybrid_index_sharded(dc, kg, comm=comm, **BUILD)
+        g = ix.export()
+        out[rank] = (g["semantic"].tobytes(), g["keyword"].idx.tobytes(), g["norm_order"].tobytes())
+        ix.close()
+        comm.close()
+        dc.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_process_sharded_build(corpus3k, world):
+    """`world` real ranks (processes), each its own CUDA context on GPU 0 and
+    its own vertex range, exchanging each pass's lists through the host
+    communicator (gloo): every rank ends with the single-process index."""
+    import torch.multiprocessing as mp
+    p, c, kg, dc = corpus3k
+    want = fg.build_hybrid_index(dc, kg, **BUILD).export()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        sem, kw, no = out[r]
+        assert sem == want["semantic"].tobytes(), r
+        assert kw == want["keyword"].idx.tobytes(), r
+        assert no == want["norm_order"].tobytes(), r
