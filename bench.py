@@ -73,6 +73,12 @@ OPERATING_POINT = {"entry": 512, "beam": 480}
 TIMED_STREAM, HELDOUT_STREAM = 0x71E5, 0x71E6
 WORKLOAD = ("configs[1]: 1M docs MS MARCO-shaped dense d=768 + learned sparse nnz 120 "
             "(vocab 30522), dense+sparse fusion, per-query weights (a, 1-a, 0, 0), a~U[0,1)")
+# configs[4] (C5): 10M docs shaped as configs[1], 100K-query batches sharded
+# over the GPUs, build sharded by vertex range.  Its operating point (recall
+# 0.9005 on one B200) is the default of `--config C5`.
+C5 = dict(docs=10_000_000, queries=100_000, point={"entry": 256, "beam": 3008},
+          workload=("configs[4]: 10M docs shaped as configs[1] (dense d=768 + learned sparse nnz 120), "
+                    "100K-query batches sharded over the GPUs, index replicated, build sharded by vertex range"))
 
 BUILD = dict(degree=32, knn_k=64, knn_iterations=10, seed=42, logical_cap=64)
 C1 = dict(docs=10000, dense_dim=128, clusters=20, cluster_spread=0.25, learned_vocab=30000,
@@ -96,7 +102,15 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-build-baseline", action="store_true")
     ap.add_argument("--make-fixture", default="", help=argparse.SUPPRESS)
-    return ap.parse_args()
+    ap.add_argument("--config", default="C2", choices=["C2", "C5"],
+                    help="C2 = configs[1] (the driver's default); C5 = configs[4] at 10M docs")
+    a = ap.parse_args()
+    if a.config == "C5":
+        if a.docs == 1_000_000:
+            a.docs = C5["docs"]
+        if a.queries == 10_000:
+            a.queries = C5["queries"]
+    return a
 
 
 def synth_params(docs):
@@ -200,8 +214,11 @@ def dist_setup(args):
     if world > 1 and args.impl != "reference":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(device_of(local))
+        if dist_backend() == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(dist_backend())
     return world, rank, local
 
 
@@ -222,7 +239,51 @@ def row_bytes(c):
 
 
 def operating_point(args):
-    return (args.entry or OPERATING_POINT["entry"]), (args.beam or OPERATING_POINT["beam"])
+    pt = C5["point"] if getattr(args, "config", "C2") == "C5" else OPERATING_POINT
+    return (args.entry or pt["entry"]), (args.beam or pt["beam"])
+
+
+def dist_backend():
+    """NCCL between GPUs; FGB_DIST_BACKEND=gloo runs several ranks on fewer
+    GPUs (multi-rank tests on a one-GPU box: ranks share device rank % GPUs,
+    the sharded build exchanges through the host communicator)."""
+    return os.environ.get("FGB_DIST_BACKEND", "nccl")
+
+
+def device_of(local):
+    import torch
+    return local % max(1, torch.cuda.device_count())
+
+
+def load_corpus(p, world, rank, group):
+    """The synthetic corpus of this run.  With several ranks on one host,
+    rank 0 generates it once into /dev/shm and the others map those arrays
+    (a 10M-doc corpus is ~41 GB of host memory per copy); FGB_BENCH_SHARED=0
+    makes every rank generate its own."""
+    from paper_2511_00855_b200 import _abi as A, synth
+    if world == 1 or os.environ.get("FGB_BENCH_SHARED", "1") == "0" or not os.path.isdir("/dev/shm"):
+        corpus, kg, _ = synth.generate_corpus(p, 0)
+        return corpus, kg, None
+    d = f"/dev/shm/fgb_corpus_{os.getppid()}_{p.docs}_{p.seed}"
+    names = ["dense", "lp", "li", "lv", "sp", "si", "sv", "kp", "ki", "ep", "ei", "doc_id", "ks", "kr", "kt"]
+    if rank == 0:
+        corpus, kg, _ = synth.generate_corpus(p, 0)
+        os.makedirs(d, exist_ok=True)
+        c = corpus
+        kw = c.keywords if c.keywords is not None else A.CSR.empty(c.n, False)
+        en = c.entities if c.entities is not None else A.CSR.empty(c.n, False)
+        for nm, x in zip(names, [c.dense, c.learned.ptr, c.learned.idx, c.learned.val, c.statistical.ptr,
+                                 c.statistical.idx, c.statistical.val, kw.ptr, kw.idx, en.ptr, en.idx, c.doc_id,
+                                 kg.source, kg.relation, kg.target]):
+            np.save(os.path.join(d, nm + ".npy"), np.asarray(x) if x is not None else np.zeros(0))
+    group.barrier()
+    if rank != 0:
+        z = {nm: np.load(os.path.join(d, nm + ".npy"), mmap_mode="r") for nm in names}
+        corpus = A.Corpus(z["dense"], A.CSR(z["lp"], z["li"], z["lv"]), A.CSR(z["sp"], z["si"], z["sv"]),
+                          A.CSR(z["kp"], z["ki"]), A.CSR(z["ep"], z["ei"]), z["doc_id"], None,
+                          p.learned_vocab, p.statistical_vocab)
+        kg = A.KG(z["ks"], z["kr"], z["kt"])
+    return corpus, kg, d
 
 
 def traffic_for(docs, entry, beam):
@@ -251,24 +312,28 @@ def main():
     import torch
     from paper_2511_00855_b200.shard import Group, build_comm, shard_range
 
-    torch.cuda.set_device(local)
-    group = Group(world, device=f"cuda:{local}")
+    dev = device_of(local)
+    torch.cuda.set_device(dev)
+    group = Group(world, device=f"cuda:{dev}" if dist_backend() == "nccl" else "cpu")
     t0 = time.time()
     p = synth_params(args.docs)
-    corpus, kg, _ = synth.generate_corpus(p, 0)
+    corpus, kg, shm_dir = load_corpus(p, world, rank, group)
     t_gen = time.time() - t0
-    comm = build_comm(world, rank, local)
+    if world > 1 and dist_backend() != "nccl":
+        comm = fg.HostComm(world, rank, dev)  # ranks sharing GPUs: host-staged exchange
+    else:
+        comm = build_comm(world, rank, dev)
     # ---- build: corpus upload + packing + build_hybrid_index (vertex-range
     # sharded over the ranks with NCCL all-gathers per pass)
     group.barrier()
     t0 = time.time()
-    dc = fg.DeviceCorpus(corpus, device=local)
+    dc = fg.DeviceCorpus(corpus, device=dev)
     t_up = time.time() - t0
     if comm is not None:
         ix = fg.build_hybrid_index_sharded(dc, kg, comm=comm, **BUILD)
     else:
         ix = fg.build_hybrid_index(dc, kg, **BUILD)
-    torch.cuda.synchronize(local)
+    torch.cuda.synchronize(dev)
     build_s = group.max(time.time() - t0)
     stages = ix.build_times()
     stages["upload"] = t_up
@@ -300,16 +365,16 @@ def main():
     for _ in range(args.warmup):
         fg.batch_query(ix, shard, entry_count=entry)
 
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     kern_ms, wall_s, scored, expanded, launches = [], [], 0, 0, 0
     res = None
     for _ in range(args.steps):
-        flush_l2(local)
+        flush_l2(dev)
         group.barrier()
-        torch.cuda.synchronize(local)
+        torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         res = fg.batch_query(ix, shard, entry_count=entry)  # H2D queries + kernel + D2H hits
-        torch.cuda.synchronize(local)
+        torch.cuda.synchronize(dev)
         wall_s.append(time.perf_counter() - t0)
         ms, nl = ix.last_search_stats()
         kern_ms.append(ms)
@@ -346,12 +411,15 @@ def main():
         "dtype": "f32 storage / f64 accumulate",
         "data": "synthetic (reference generate_corpus, bit-identical), seed 1",
         "config": {
-            "workload": WORKLOAD,
+            "workload": C5["workload"] if args.config == "C5" else WORKLOAD,
             "docs": corpus.n, "queries_per_step": queries.count, "queries_per_gpu": hi - lo,
             "k": 10, "beam": beam, "entry_count": entry, "build": BUILD,
             "operating_point": "held-out selection (bench.py --sweep, stream 0x71E6)"
                                if not (args.beam or args.entry) else "forced by --beam/--entry",
-            "parallelism": f"query-shard x{world}, index replicated; build vertex-range x{world} (NCCL all-gather)",
+            "parallelism": f"query-shard x{world}, index replicated; build vertex-range x{world} "
+                           f"({'NCCL' if dist_backend() == 'nccl' or world == 1 else 'host-staged ' + dist_backend()} "
+                           f"all-gather)" + ("" if world <= torch.cuda.device_count()
+                                             else f"; {world} ranks share {torch.cuda.device_count()} GPU(s)"),
             "l2": "flushed (256 MiB write) before each timed step; corpus 4 GB > L2",
         },
         "recall_at_10": round(recall, 4) if recall is not None else None,
@@ -388,6 +456,10 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
+        group.barrier()
+        if rank == 0 and shm_dir:  # every rank has uploaded its copy long ago
+            import shutil
+            shutil.rmtree(shm_dir, ignore_errors=True)
         dist.destroy_process_group()
 
 
