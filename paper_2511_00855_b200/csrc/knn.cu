@@ -1077,11 +1077,14 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
 
 uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s, ReverseLists& R, DevKnn& next,
                             DevBuf<unsigned long long>& changed) {
+    HostTimer ht("knn_iterate");
     knn_reverse_lists(g, R, s);
+    ht.mark("reverse lists");
     if (next.n != g.n || next.k != g.k) next.alloc(g.n, g.k);
     if (changed.size() != 1) changed.alloc(1);
     changed.zero(s);
     knn_pass_range(c, g, R, 0, g.n, next, changed.get(), s);
+    ht.mark("pass kernel");
     unsigned long long h_changed = 0;
     changed.download(&h_changed, 1, s);
     FGB_CUDA(cudaStreamSynchronize(s));
