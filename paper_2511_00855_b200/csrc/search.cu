@@ -1133,7 +1133,7 @@ bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunc
     h.lccap = std::max(ix->max_logical_group, 1u);
     const uint32_t list_max = ix->degree + (any_req ? ix->max_kw_edges : 0) + (any_ctx ? h.lccap : 0);
     h.seencap = 64;
-    while (h.seencap < 2 * list_max) h.seencap <<= 1;
+    while (2 * h.seencap < 3 * list_max) h.seencap <<= 1;  // load <= 2/3
     if (hybrid_warp_smem(h) == 0) return false;
     const uint64_t all_slots = hybrid_slots(h, nq, c.device);
     h.p.hit_stride = stride;

@@ -51,6 +51,7 @@ using approx::kSG;
 using approx::sparse_group;
 constexpr int kMinWarps = 10;  // launch bound: query-warps per SM (register budget)
 constexpr uint32_t kXq = 64;   // exact re-score requests per certification round
+constexpr uint32_t kStage = 64;  // staged offers (< 32 carried + one window of 32)
 enum : uint32_t { QF_VALID = 1, QF_ENTITY = 2, QF_FALLBACK = 4 };
 
 struct HybridMem {
@@ -68,6 +69,11 @@ struct HybridMem {
     uint32_t* xi;    //   cand position (pool entries)
     double* xd;      //   result
     unsigned long long* ph;  // phase timing slots
+    // offers staged across the windows of one neighbour list (reach order):
+    // windows with few new nodes (keyword / logical tails) share a batch
+    uint4* st_meta;
+    uint32_t* st_node;
+    uint32_t* st_fl;  // assigned hop | improved << 31
 };
 
 __device__ __forceinline__ HybridMem carve(unsigned char* base, const HybridLaunch& h) {
@@ -94,6 +100,9 @@ __device__ __forceinline__ HybridMem carve(unsigned char* base, const HybridLaun
     m.xn = reinterpret_cast<uint32_t*>(take(kXq * 4));
     m.xi = reinterpret_cast<uint32_t*>(take(kXq * 4));
     m.ph = reinterpret_cast<unsigned long long*>(take(kHybCount * 8));
+    m.st_meta = reinterpret_cast<uint4*>(take(kStage * 16));
+    m.st_node = reinterpret_cast<uint32_t*>(take(kStage * 4));
+    m.st_fl = reinterpret_cast<uint32_t*>(take(kStage * 4));
     return m;
 }
 
@@ -102,7 +111,7 @@ size_t carve_bytes(const HybridLaunch& h) {
     return al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0])) + al16(path_bytes(a.vocab[1], a.cap[1])) +
            al16(a.beamcap * 8) + al16(a.kcap * 8) + al16(a.beamcap * 4) + al16(a.kcap * 4) + al16(32 * 4) +
            al16(h.reqcap * 4 + 4) + al16(h.lccap * 8 + 8) + al16(h.seencap * 4) + al16(kXq * 8) + 2 * al16(kXq * 4) +
-           al16(kHybCount * 8);
+           al16(kHybCount * 8) + al16(kStage * 16) + 2 * al16(kStage * 4);
 }
 
 // ---------------------------------------------------------------- helpers
@@ -327,9 +336,13 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
         uint64_t kwb = 0;
         bool propagate = false, multi = false;
 
+        uint32_t nst = 0;  // offers staged (w.st_*), in reach order
 #pragma unroll 1
         while (err == 0) {
             mark(kHybTopk);  // (the previous batch's top-k step)
+            // leftovers of a finished list are scored before the next selection
+            const bool drain = nst > 0 && seed_next >= nseeds && adj_b >= L;
+            if (!drain) {
             uint32_t node = 0, sent = 0;
             uint4 nm = make_uint4(0, 0, 0, 0);
             bool v = false, is_seed = false;
@@ -499,22 +512,40 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
                 scored += __popc(frm);
             }
             const uint32_t fm = __ballot_sync(kFull, fresh || improved);
+            if (fresh || improved) {  // stage the offers in reach order
+                const uint32_t pos = nst + __popc(fm & lt);
+                w.st_node[pos] = node;
+                w.st_meta[pos] = nm;
+                w.st_fl[pos] = ahop | (improved ? 0x80000000u : 0u);
+            }
+            nst += __popc(fm);
+            __syncwarp();
             mark(kHybVisit);
-            if (!fm) continue;
+            // score once a batch is full or the list (seeds / expansion) ends
+            if (nst == 0 || (nst < 32 && !(seed_next >= nseeds && adj_b >= L))) continue;
+            }  // (!drain)
 
-            // ---- score the F offered nodes (new or improved), compacted into lanes 0..F-1
-            const uint32_t F = __popc(fm);
-            const uint32_t src = __fns(fm, 0, lane + 1);
-            const uint32_t sl = src < 32 ? src : 0;
-            const uint32_t cn = __shfl_sync(kFull, node, sl);
-            uint4 mt;
-            mt.x = __shfl_sync(kFull, nm.x, sl);
-            mt.y = __shfl_sync(kFull, nm.y, sl);
-            mt.z = __shfl_sync(kFull, nm.z, sl);
-            mt.w = __shfl_sync(kFull, nm.w, sl);
-            const uint32_t chop = __shfl_sync(kFull, ahop, sl);
-            const bool cimp = __shfl_sync(kFull, improved, sl);
+            // ---- score the F staged offers (new or improved nodes) in lanes 0..F-1
+            const uint32_t F = min(nst, 32u);
             const bool mine = lane < F;
+            uint32_t cn = 0, chop = 0;
+            uint4 mt = make_uint4(0, 0, 0, 0);
+            bool cimp = false;
+            if (mine) {
+                cn = w.st_node[lane];
+                mt = w.st_meta[lane];
+                const uint32_t fl = w.st_fl[lane];
+                chop = fl & 0x7FFFFFFFu;
+                cimp = (fl >> 31) != 0;
+            }
+            __syncwarp();
+            if (nst > F && lane < nst - F) {  // carry the rest (< 32) to the front
+                w.st_node[lane] = w.st_node[F + lane];
+                w.st_meta[lane] = w.st_meta[F + lane];
+                w.st_fl[lane] = w.st_fl[F + lane];
+            }
+            __syncwarp();
+            nst -= F;
             const double rew = (mine && chop) ? rtab[chop - 1] : 0.0;
             if (mine && (a.prefetch & 4)) {
 #pragma unroll
