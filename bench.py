@@ -198,6 +198,55 @@ def peak_hbm():
         return 6650.0, "fallback"
 
 
+def peak_bf16():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    except Exception:
+        return 1590.0, "fallback"
+
+
+def build_rooflines(fg, ix, corpus, stages):
+    """Rooflines of the two construction kernels from this build's own
+    counters: NN-Descent (algorithmic bytes = pair scores x row bytes, SURVEY
+    8(d); the bytes the certified screening actually gathers beside it) and
+    the refinery's tensor-core Gram (useful dense FLOPs = pairs x 2d)."""
+    bs = ix.build_stats()
+    R = row_bytes(corpus)
+    peak, kind = peak_hbm()
+    out = {}
+    if bs["pass_seconds"] > 0:
+        nl = corpus.learned.ptr[-1] / corpus.n
+        ns = corpus.statistical.ptr[-1] / corpus.n
+        gathered = bs["candidates"] * 8 * (nl + ns) + bs["dense_rows"] * 4 * corpus.dense_dim
+        alg = bs["candidates"] * R
+        out["knn"] = {
+            "bound": "hbm", "kernel": "knn_pass_kernel", "passes": bs["passes"], "pair_scores": bs["candidates"],
+            "dense_rows_read": bs["dense_rows"], "device_seconds": round(bs["pass_seconds"], 3),
+            "alg_bytes": int(alg), "achieved": round(alg / bs["pass_seconds"] / 1e9, 1), "peak": peak,
+            "peak_kind": kind, "unit": "GB/s", "frac": round(alg / bs["pass_seconds"] / 1e9 / peak, 4),
+            "gathered_bytes": int(gathered),
+            "gathered_frac": round(gathered / bs["pass_seconds"] / 1e9 / peak, 4),
+            "traffic_note": "pass 1 at 200K docs under ncu: 2.75 TB DRAM in 1.05 s = 0.40 of peak "
+                            "(profiles/r02_knn_pass1_ncu.md)",
+            "note": "alg_bytes counts every scored pair at full row bytes; the certified screening reads the "
+                    "dense row of only dense_rows_read of them"}
+    tc = fg.refine_tc_stats(reset=True)
+    if tc["pairs"]:
+        flops = tc["pairs"] * 2.0 * corpus.dense_dim
+        tpk, tkind = peak_bf16()
+        out["refine_gram"] = {
+            "bound": "tensor", "kernel": "refine_node_kernel (tcgen05 split-bf16 Gram)", "pairs": tc["pairs"],
+            "exact_rescored": tc["resolved"], "useful_dense_tflop": round(flops / 1e12, 3),
+            "refine_seconds": round(stages.get("refine", 0.0), 3),
+            "achieved": round(flops / max(stages.get("refine", 1e-9), 1e-9) / 1e12, 2), "peak": tpk,
+            "peak_kind": tkind, "unit": "TFLOP/s",
+            "frac": round(flops / max(stages.get("refine", 1e-9), 1e-9) / 1e12 / tpk, 5),
+            "note": "one 64x64x768 Gram per node (x3 MMAs for the hi/lo split): the refine stage is bound by "
+                    "the sparse merge-joins, not the tensor pipe (profiles/r02_refine_tc.md)"}
+    return out
+
+
 def cpu_model():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -326,6 +375,7 @@ def main():
         comm = build_comm(world, rank, dev)
     # ---- build: corpus upload + packing + build_hybrid_index (vertex-range
     # sharded over the ranks with NCCL all-gathers per pass)
+    os.environ.setdefault("FGB_REFINE_TC_STATS", "1")  # counters for the build roofline (a few atomics)
     group.barrier()
     t0 = time.time()
     dc = fg.DeviceCorpus(corpus, device=dev)
@@ -338,6 +388,7 @@ def main():
     build_s = group.max(time.time() - t0)
     stages = ix.build_times()
     stages["upload"] = t_up
+    build_roof = build_rooflines(fg, ix, corpus, stages)
 
     queries = c2_queries(p, args.queries, TIMED_STREAM)
     entry, beam = operating_point(args)
@@ -442,6 +493,7 @@ def main():
                      "per_query": {"scored": scored / max(shard.count, 1),
                                    "expanded": expanded / max(shard.count, 1), "row_bytes": R}},
         "clocks": clk,
+        "build_roofline": build_roof,
     }
     if sweep is not None:
         line["sweep"] = {"queries": args.eval_queries, "stream": HELDOUT_STREAM, "points": sweep}

@@ -311,6 +311,11 @@ int fg_index_export(const fg_index* ix, uint32_t* semantic, uint64_t* keyword_pt
 /* Seconds spent in the last fg_index_build, split by stage (may be NULL):
  * [0] knn, [1] refine, [2] logical+entity map, [3] norm order, [4] total. */
 int fg_index_build_times(const fg_index* ix, double* seconds5);
+/* NN-Descent totals of fg_index_build: {passes, candidate pair scores (the
+ * sum over passes and nodes of S_u, knn_graph.cpp:122-131), dense rows read
+ * after the certified screening, device microseconds of the pass kernels};
+ * zeros for other builds.  Feeds the build roofline of bench.py. */
+int fg_index_build_stats(const fg_index* ix, uint64_t* stats4);
 int fg_index_free(fg_index* ix);
 
 /* InsertParams (update.hpp:22-28). */

@@ -621,6 +621,13 @@ int fg_index_insert(fg_index* ix, const fg_corpus_view* docs, const fg_insert_pa
 }
 
 
+int fg_index_build_stats(const fg_index* ix, uint64_t* stats4) {
+    return guarded([&] {
+        if (!ix || !stats4) throw Error("invalid-argument", "null pointer");
+        for (int i = 0; i < 4; ++i) stats4[i] = ix->knn_stats[i];
+    });
+}
+
 int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p, fg_index** out) {
     return guarded([&] {
         if (!c || !p || !out) throw Error("invalid-argument", "null pointer");
@@ -644,7 +651,12 @@ int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p,
         auto t0 = Clock::now();
         DevKnn g;
         HostTimer ht("index_build");
-        knn_build_device(*c, p->knn_k, p->knn_iterations, 0.01, p->seed, g, s);
+        KnnStats ks;
+        knn_build_device(*c, p->knn_k, p->knn_iterations, 0.01, p->seed, g, s, &ks);
+        ix->knn_stats[0] = ks.passes;
+        ix->knn_stats[1] = ks.candidates;
+        ix->knn_stats[2] = ks.dense_rows;
+        ix->knn_stats[3] = static_cast<uint64_t>(ks.pass_seconds * 1e6);
         FGB_CUDA(cudaStreamSynchronize(s));
         ix->build_seconds[0] = secs(t0);
 

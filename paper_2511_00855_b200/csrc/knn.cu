@@ -138,6 +138,7 @@ struct PassArgs {
     uint32_t pshift;    // part of id = (id * 0x9E3779B1) >> pshift
     unsigned int* overflow;  // pool overflow counter (0 after a correct pass)
     const uint32_t* order;   // CTA b processes node order[lo + b] (graph locality); nullptr: lo + b
+    unsigned long long* counts;  // [0] candidates scored (sum of S_u), [1] dense rows read
 };
 
 enum : int {
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     auto count = [&](int slot, uint32_t v) {
         if (a.timing && v) atomicAdd(&a.timing[slot], static_cast<unsigned long long>(v));
     };
+    uint32_t cand_total = 0, dense_rows = 0;  // (thread 0 / lane 0 of each warp)
 
     for (uint32_t j = tid; j < k; j += nt) {
         T_id[j] = a.L_ids[u * k + j];
@@ -598,6 +600,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     }
     __syncthreads();
     const uint32_t n_c = n_cand;
+    cand_total += n_c;
     uint32_t round = 0;
     for (uint32_t base = 0; base < n_c; ++round) {
       const uint32_t grow = part > 0 ? uint32_t(kSRounds) : round == 0 ? 1u : round == 1 ? 2u : uint32_t(kSRounds);
@@ -641,6 +644,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
                 if (lane == 0) {
                     count(kKnCand, F);
                     count(kKnDense, __popc(km));
+                    dense_rows += __popc(km);
                 }
                 const double D = approx::dense_group<NQ4, 2>(a.c, qd, cn, lane, km);
                 const double v = __dadd_rn(__dadd_rn(D, L), S);
@@ -821,6 +825,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     mine = __reduce_add_sync(0xFFFFFFFFu, mine);
     if ((tid & 31) == 0 && mine) atomicAdd(a.changed, (unsigned long long)mine);
     lap(kKnPhFinal);
+    if (a.counts) {
+        if (tid == 0) atomicAdd(&a.counts[0], static_cast<unsigned long long>(cand_total));
+        if (lane == 0 && dense_rows) atomicAdd(&a.counts[1], static_cast<unsigned long long>(dense_rows));
+    }
 }
 
 size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap,
@@ -984,7 +992,8 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     PassArgs a{c.dc,           k,           g.ids.get(),   g.scores.get(), g.fresh.get(),
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, 0, lcap, scap, lo,
-               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin, 1, 32, nullptr, nullptr};
+               0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin, 1, 32, nullptr, nullptr, nullptr};
+    if (R.counts.size() == 2) a.counts = R.counts.get();
     // (results do not depend on the order nodes are processed in)
     if (R.order.size() == g.n && lo == 0 && hi == g.n) a.order = R.order.get();
     if (const char* e = std::getenv("FGB_KNN_SORT_MIN")) a.sort_min = std::max(1, std::atoi(e));
@@ -1083,11 +1092,20 @@ uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s, Rever
     if (next.n != g.n || next.k != g.k) next.alloc(g.n, g.k);
     if (changed.size() != 1) changed.alloc(1);
     changed.zero(s);
+    if (!R.ev0) {
+        FGB_CUDA(cudaEventCreate(&R.ev0));
+        FGB_CUDA(cudaEventCreate(&R.ev1));
+    }
+    FGB_CUDA(cudaEventRecord(R.ev0, s));
     knn_pass_range(c, g, R, 0, g.n, next, changed.get(), s);
+    FGB_CUDA(cudaEventRecord(R.ev1, s));
     ht.mark("pass kernel");
     unsigned long long h_changed = 0;
     changed.download(&h_changed, 1, s);
     FGB_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    FGB_CUDA(cudaEventElapsedTime(&ms, R.ev0, R.ev1));
+    R.pass_ms += ms;
     std::swap(g.ids, next.ids);  // the old snapshot's buffers serve the next pass
     std::swap(g.scores, next.scores);
     std::swap(g.fresh, next.fresh);
@@ -1133,7 +1151,7 @@ void locality_order(const DevKnn& g, DevBuf<uint32_t>& order, cudaStream_t s) {
 }
 
 uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
-                          double convergence, uint64_t seed, DevKnn& g, cudaStream_t s) {
+                          double convergence, uint64_t seed, DevKnn& g, cudaStream_t s, KnnStats* stats) {
     uint32_t k = k_req;
     if (c.n >= 2 && k >= c.n) k = static_cast<uint32_t>(c.n - 1);  // knn_graph.cpp:153-156
     HostTimer ht("knn_build");
@@ -1142,6 +1160,10 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
     const double denom = static_cast<double>(c.n) * k;
     uint32_t passes = 0;
     ReverseLists R;
+    if (stats) {
+        R.counts.alloc(2);
+        R.counts.zero(s);
+    }
     DevKnn next;
     DevBuf<unsigned long long> d_changed;
     for (uint32_t it = 0; it < max_iterations; ++it) {
@@ -1157,6 +1179,15 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
             locality_order(g, R.order, s);
             ht.mark("order");
         }
+    }
+    if (stats) {
+        unsigned long long h[2] = {0, 0};
+        R.counts.download(h, 2, s);
+        FGB_CUDA(cudaStreamSynchronize(s));
+        stats->passes = passes;
+        stats->candidates = h[0];
+        stats->dense_rows = h[1];
+        stats->pass_seconds = R.pass_ms / 1e3;
     }
     return passes;
 }

@@ -34,6 +34,26 @@ struct ReverseLists {
     // node visiting order of the pass kernel (graph locality, set after
     // pass 1 by knn_build_device; empty: identity)
     DevBuf<uint32_t> order;
+    // pass statistics (knn_build_device with a KnnStats): candidate / dense
+    // row counters, device time of the pass kernels
+    DevBuf<unsigned long long> counts;
+    double pass_ms = 0.0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ReverseLists() = default;
+    ReverseLists(const ReverseLists&) = delete;
+    ReverseLists& operator=(const ReverseLists&) = delete;
+    ~ReverseLists() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+};
+
+// NN-Descent totals over a build: passes, candidates scored (sum over passes
+// and nodes of S_u, the fresh new two-hop candidates), dense rows read after
+// screening, device seconds of the pass kernels.
+struct KnnStats {
+    uint64_t passes = 0, candidates = 0, dense_rows = 0;
+    double pass_seconds = 0.0;
 };
 
 // init_random_graph (knn_graph.cpp:52-73) into g (allocated n x k).
@@ -49,7 +69,7 @@ uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s, Rever
                             DevBuf<unsigned long long>& changed);
 // build_knn_graph (knn_graph.cpp:150-166); returns the number of passes run.
 uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_iterations,
-                          double convergence, uint64_t seed, DevKnn& g, cudaStream_t s);
+                          double convergence, uint64_t seed, DevKnn& g, cudaStream_t s, KnnStats* stats = nullptr);
 
 struct RefineOut {
     uint32_t degree = 0, k = 0;

@@ -227,6 +227,11 @@ class HybridIndex:
         check(lib().fg_index_build_times(self.h, A.ptr(t, A.f64p)))
         return dict(knn=t[0], refine=t[1], logical=t[2], norm_order=t[3], total=t[4])
 
+    def build_stats(self) -> dict:
+        t = np.zeros(4, np.uint64)
+        check(lib().fg_index_build_stats(self.h, A.ptr(t, A.u64p)))
+        return dict(passes=int(t[0]), candidates=int(t[1]), dense_rows=int(t[2]), pass_seconds=int(t[3]) / 1e6)
+
     def last_search_stats(self):
         ms, launches = C.c_double(), C.c_uint64()
         check(lib().fg_last_search_stats(self.h, C.byref(ms), C.byref(launches)))
