@@ -1129,6 +1129,7 @@ bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunc
     h.kg_nbr = ix->kg_nbr.get();
     h.kg_rows = ix->kg_rows;
     h.conjunctive = conj ? 1 : 0;
+    h.variant = any_ctx && !any_req ? kHybCtx : (any_req && !any_ctx ? kHybReq : kHybBoth);
     h.reqcap = std::max(max_req, 1u);
     h.lccap = std::max(ix->max_logical_group, 1u);
     const uint32_t list_max = ix->degree + (any_req ? ix->max_kw_edges : 0) + (any_ctx ? h.lccap : 0);

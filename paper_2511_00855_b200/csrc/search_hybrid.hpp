@@ -37,7 +37,12 @@ struct HybridLaunch {
     const uint32_t* qlist;         // optional subset of query ids (overflow re-runs)
     uint32_t qlist_n;
     unsigned long long* timing;    // optional phase cycles (FGB_SEARCH_TIMING=1), kHyb* slots
+    uint32_t variant;              // kHybBoth / kHybCtx / kHybReq: the instantiation to run
 };
+
+// Kernel instantiations by the batch's features: entity context only,
+// required keywords only, or both (also forced plain batches).
+enum : uint32_t { kHybBoth = 0, kHybCtx = 1, kHybReq = 2 };
 
 enum : int {
     kHybSelect = 0, kHybList, kHybVisit, kHybSparse, kHybDense, kHybCand, kHybTopk, kHybFinal,
