@@ -310,3 +310,56 @@ def test_search_scratch_overflow_reruns(kg_case, ref, monkeypatch):
     q.required = A.CSR.from_rows([q.statistical.row(i)[0][:1].tolist() for i in range(q.count)])
     for conj in (True, False):
         _same_results(fg.batch_query(gix, q, conjunctive=conj), ref.batch_query(rix, q, conjunctive=conj))
+
+
+def _chain_batch(chains, went, beam, hops, k=10):
+    dense = np.stack([ch.query_dense for ch in chains])
+    learned = A.CSR.from_rows([ch.query_learned[0] for ch in chains], [ch.query_learned[1] for ch in chains])
+    stat = A.CSR.from_rows([ch.query_statistical[0] for ch in chains], [ch.query_statistical[1] for ch in chains])
+    w = np.tile(np.array([[1, 1, 1, went]], np.float32), (len(chains), 1))
+    ents = A.CSR.from_rows([[ch.e0] for ch in chains])
+    return A.Queries(dense, learned, stat, w, k=k, beam_width=beam, max_entity_hops=hops, entities=ents)
+
+
+@pytest.mark.parametrize("hops,beam,k", [(0, 64, 10), (1, 10, 10), (5, 48, 10), (2, 200, 25)])
+def test_search_entities_hops_and_beams(kg_case, ref, hops, beam, k):
+    """search_hybrid_kernel edge cases: no propagation (hops 0), beam == k,
+    deep hop caps, k > 10 with a wide beam."""
+    p, c, kg, chains, dev, gix, rix = kg_case
+    q = _chain_batch(chains, 100.0, beam, hops, k)
+    g = fg.batch_query(gix, q)
+    assert gix.last_search_kernel() == "search_hybrid_kernel"
+    _same_results(g, ref.batch_query(rix, q))
+
+
+def test_search_keyword_shortfall_and_absent_terms(kg_case, ref):
+    """Required terms that no document carries (every result filtered:
+    keyword-shortfall warnings) next to ordinary keyword queries."""
+    p, c, kg, chains, dev, gix, rix = kg_case
+    q = synth.synth_queries(p, 24, beam_width=32)
+    rows = []
+    for i in range(q.count):
+        si, _ = q.statistical.row(i)
+        rows.append([10 ** 6 + i] if i % 3 == 0 else sorted(si[:1 + i % 2].tolist()))
+    q.required = A.CSR.from_rows(rows)
+    for conj in (True, False):
+        g = fg.batch_query(gix, q, conjunctive=conj)
+        _same_results(g, ref.batch_query(rix, q, conjunctive=conj))
+        assert np.any(g.warnings & 2)
+
+
+def test_search_entities_with_deleted_seeds(kg_case, ref):
+    """Entity seeds that are deleted stay routable but never reach results."""
+    p, c, kg, chains, dev, gix, rix = kg_case
+    g_graph = ref.index_export(rix, c.n)
+    flags = np.zeros(c.n, np.uint8)
+    seed_nodes = [int(n) for ch in chains for n in np.nonzero([ch.e0 in c.entities.row(i)[0]
+                                                               for i in range(c.n)])[0][:1]]
+    flags[seed_nodes] = 1
+    flags[np.random.default_rng(8).choice(c.n, 100, replace=False)] = 1
+    cd = A.Corpus(c.dense, c.learned, c.statistical, c.keywords, c.entities, c.doc_id, flags)
+    dev2 = fg.DeviceCorpus(cd)
+    gix2 = fg.HybridIndex.from_graph(dev2, g_graph, kg)
+    rix2 = ref.index_create(ref.store(cd, kg), g_graph, 16)
+    q = _chain_batch(chains, 100.0, 64, 2)
+    _same_results(fg.batch_query(gix2, q), ref.batch_query(rix2, q))
