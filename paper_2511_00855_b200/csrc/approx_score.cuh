@@ -39,12 +39,26 @@ struct PathQ {
     const float* vals;
     const uint32_t* filt;
     uint32_t mask;
+    uint32_t hm1, hm2, hshift;  // cuckoo layout: slots (t * hm1) >> hshift and (t * hm2) >> hshift
 };
 
+// Lookup layouts: filter + open-addressing hash (0), bitmap + rank (1),
+// two-choice cuckoo table (2: branch-free, exactly two probes).
+enum : int { kLookHash = 0, kLookBitmap = 1, kLookCuckoo = 2 };
+
 // The weighted query value of term t (found=false, 0 when absent).
-template <bool kBitmap>
+template <int kLook>
 __device__ __forceinline__ float q_lookup_t(const PathQ& P, uint32_t t, bool& found) {
-    if constexpr (kBitmap) {
+    if constexpr (kLook == kLookCuckoo) {
+        // both candidate slots always probed: no divergence between lanes
+        const uint32_t s1 = (t * P.hm1) >> P.hshift, s2 = (t * P.hm2) >> P.hshift;
+        const uint32_t k1 = P.keys[s1], k2 = P.keys[s2];
+        const bool h1 = k1 == t, h2 = k2 == t;
+        found = (h1 || h2) && t != kPad;
+        float q = 0.0f;
+        if (found) q = P.vals[h1 ? s1 : s2];
+        return q;
+    } else if constexpr (kLook == kLookBitmap) {
         // the bitmap spans a power of two of words past the vocabulary, so
         // masking maps the padding id (0xFFFFFFFF) to a bit that is never set
         const uint32_t tw = (t >> 5) & P.wm1;
@@ -62,20 +76,22 @@ __device__ __forceinline__ float q_lookup_t(const PathQ& P, uint32_t t, bool& fo
 }
 
 __device__ __forceinline__ float q_lookup(const PathQ& P, uint32_t t, bool& found) {
-    return P.vocab ? q_lookup_t<true>(P, t, found) : q_lookup_t<false>(P, t, found);
+    return P.vocab ? q_lookup_t<kLookBitmap>(P, t, found) : q_lookup_t<kLookHash>(P, t, found);
 }
 
 // Lookup modes of a search kernel instantiation: every active sparse path of
 // the batch uses the hash (0) or the bitmap (1), or each path its own (2).
 // One mode per instantiation keeps a single lookup variant in the hot loop
 // (instruction-cache footprint).
-enum : int { kModeHash = 0, kModeBitmap = 1, kModeMixed = 2 };
+enum : int { kModeHash = 0, kModeBitmap = 1, kModeMixed = 2, kModeCuckoo = 3 };
 template <int kMode>
 __device__ __forceinline__ float q_lookup_m(const PathQ& P, uint32_t t, bool& found) {
     if constexpr (kMode == kModeBitmap)
-        return q_lookup_t<true>(P, t, found);
+        return q_lookup_t<kLookBitmap>(P, t, found);
     else if constexpr (kMode == kModeHash)
-        return q_lookup_t<false>(P, t, found);
+        return q_lookup_t<kLookHash>(P, t, found);
+    else if constexpr (kMode == kModeCuckoo)
+        return q_lookup_t<kLookCuckoo>(P, t, found);
     else
         return q_lookup(P, t, found);
 }
@@ -87,7 +103,7 @@ __device__ __forceinline__ float q_lookup_m(const PathQ& P, uint32_t t, bool& fo
 // once — |error| <= gamma_4 (fp32) * sum|q_i v_i| <= gamma_4 |q_sparse| |d|,
 // which the caller's bound must carry (knn.cu; the search keeps fp64: its
 // tighter bound resolves 14x fewer comparisons exactly).
-template <bool kBitmap, bool kF32 = false>
+template <int kBitmap, bool kF32 = false>
 __device__ __forceinline__ double probe4(const uint4& ii, const float4& vv, const PathQ& P) {
     bool f0, f1, f2, f3;
     const float q0 = q_lookup_t<kBitmap>(P, ii.x, f0), q1 = q_lookup_t<kBitmap>(P, ii.y, f1);
@@ -135,7 +151,7 @@ __device__ __forceinline__ double reduce_scatter8(double (&x)[8], uint32_t lane)
 // by lanes 0..F-1 ((off4, nnz) each); lane j receives node j's sum.  kSG
 // nodes' first 128 postings (idx + val, coalesced 512 B each) are in flight
 // per round trip; postings 128.. of longer rows follow in a rolled loop.
-template <bool kBitmap, bool kF32 = false>
+template <int kBitmap, bool kF32 = false>
 __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float* val, const PathQ P, uint32_t off4,
                                             uint32_t nnz, uint32_t lane, uint32_t F) {
     double mine = 0.0;
@@ -167,6 +183,7 @@ __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float*
         PathQ Pg = P;
         Pg.wm1 = min(P.wm1, P.wm1 | tok);
         Pg.mask = min(P.mask, P.mask | tok);
+        if constexpr (kBitmap == kLookCuckoo) Pg.hshift = min(P.hshift, P.hshift | tok);
         double part[8];
 #pragma unroll
         for (int k = 0; k < kSG; ++k) part[k] = probe4<kBitmap, kF32>(ii[k], vv[k], Pg);

@@ -235,8 +235,11 @@ __device__ __forceinline__ uint32_t pool_insert(const Pool& p, uint32_t& size, d
 
 __host__ __device__ __forceinline__ size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
 
-// Bytes of one staged sparse path (PlainLaunch::vocab/cap).
-__host__ __device__ __forceinline__ size_t path_bytes(uint32_t vocab, uint32_t cap) {
+// Bytes of one staged sparse path (PlainLaunch::vocab/cap; cuckoo: a
+// two-choice table of cap slots, cap >= 4 x the query's terms, plus the
+// term list it is built from).
+__host__ __device__ __forceinline__ size_t path_bytes(uint32_t vocab, uint32_t cap, bool cuckoo = false) {
+    if (cuckoo) return 2 * al16(cap * 4) + al16(cap * 2);
     if (vocab) {
         const size_t W = approx::bitmap_words(vocab);
         return al16(W * 4) + al16(W * 2) + al16(cap * 4);
@@ -246,8 +249,14 @@ __host__ __device__ __forceinline__ size_t path_bytes(uint32_t vocab, uint32_t c
 
 // Stages sparse path `path` of query qi (build_query_vector: fp32 w * v,
 // a zero weight drops the path, corpus.cpp:86-103); returns sum of (w v)^2.
+// Odd multipliers of the cuckoo tables, tried in order until every query
+// term has a slot (a table at <= 1/4 load practically never needs the second).
+__device__ __constant__ const uint32_t kCuckooMul[8][2] = {
+    {0x9E3779B1u, 0x85EBCA77u}, {0xC2B2AE3Du, 0x27D4EB2Fu}, {0x165667B1u, 0xD3A2646Du}, {0xFD7046C5u, 0xB55A4F09u},
+    {0x2545F491u, 0x4F1BBCDDu}, {0x68E31DA5u, 0x1B873593u}, {0xCC9E2D51u, 0x7FEB352Du}, {0x846CA68Bu, 0xE6546B65u}};
+
 __device__ inline double stage_path(const DevQueries& q, const uint32_t* vocabs, const uint32_t* caps, uint64_t qi, int path,
-                             unsigned char* mem, PathQ& P, uint32_t lane) {
+                             unsigned char* mem, PathQ& P, uint32_t lane, bool cuckoo = false) {
     const uint64_t lb = path ? q.s_ptr[qi] : q.l_ptr[qi], le = path ? q.s_ptr[qi + 1] : q.l_ptr[qi + 1];
     const uint32_t* qidx = path ? q.s_idx : q.l_idx;
     const float* qval = path ? q.s_val : q.l_val;
@@ -296,6 +305,62 @@ __device__ inline double stage_path(const DevQueries& q, const uint32_t* vocabs,
             if (t < vocab) qv[pre[t >> 5] + __popc(bm[t >> 5] & ((1u << (t & 31)) - 1u))] = v;
         }
         __syncwarp();
+        return ss;
+    }
+    if (cuckoo) {
+        // two-choice cuckoo table: every lookup probes exactly two slots (no
+        // data-dependent probe loop, so lanes of a warp never diverge on it)
+        uint32_t* keys = reinterpret_cast<uint32_t*>(mem);
+        float* vals = reinterpret_cast<float*>(mem + al16(cap * 4));
+        uint32_t* tk = reinterpret_cast<uint32_t*>(mem + 2 * al16(cap * 4));
+        float* tv = reinterpret_cast<float*>(tk + cap / 4);
+        P.keys = keys;
+        P.vals = vals;
+        P.mask = cap - 1;
+        P.hshift = 32u - static_cast<uint32_t>(__ffs(cap) - 1);
+        P.hm1 = P.hm2 = 1u;
+        if (!P.on) return 0.0;
+        const uint32_t nt = static_cast<uint32_t>(le - lb);  // <= cap / 4 (host)
+        for (uint64_t j = lb + lane; j < le; j += 32) {
+            const float v = __fmul_rn(wt, qval[j]);
+            ss += (double)v * (double)v;
+            tk[j - lb] = qidx[j];
+            tv[j - lb] = v;
+        }
+        bool ok = false;
+        for (int seed = 0; seed < 8 && !ok; ++seed) {
+            const uint32_t m1 = kCuckooMul[seed][0], m2 = kCuckooMul[seed][1], sh = P.hshift;
+            for (uint32_t j = lane; j < cap; j += 32) keys[j] = kEmpty;
+            __syncwarp();
+            uint32_t good = 1;
+            if (lane == 0) {
+                for (uint32_t j = 0; j < nt && good; ++j) {
+                    uint32_t key = tk[j];
+                    float val = tv[j];
+                    uint32_t pos = (key * m1) >> sh;
+                    good = 0;
+                    for (uint32_t kick = 0; kick < 4 * nt + 16; ++kick) {
+                        const uint32_t old = keys[pos];
+                        const float oldv = vals[pos];
+                        keys[pos] = key;
+                        vals[pos] = val;
+                        if (old == kEmpty) {
+                            good = 1;
+                            break;
+                        }
+                        key = old;
+                        val = oldv;
+                        const uint32_t p1 = (key * m1) >> sh;
+                        pos = pos == p1 ? (key * m2) >> sh : p1;
+                    }
+                }
+            }
+            ok = __shfl_sync(kFull, good, 0) != 0;
+            P.hm1 = m1;
+            P.hm2 = m2;
+            __syncwarp();
+        }
+        if (!ok) P.hm1 = 0;  // no table found: the caller fails the query
         return ss;
     }
     uint32_t* keys = reinterpret_cast<uint32_t*>(mem);

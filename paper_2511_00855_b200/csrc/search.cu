@@ -1429,6 +1429,19 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                 const bool all_hash = (!l_on || !pl.vocab[0]) && (!s_on || !pl.vocab[1]);
                 pl.mode = all_hash ? approx::kModeHash : approx::kModeMixed;
                 if (const char* e = std::getenv("FGB_SEARCH_MODE"); e && e[0] == '2') pl.mode = approx::kModeMixed;
+                // hash batches: two-choice cuckoo tables (FGB_SEARCH_CUCKOO=0: filter + hash)
+                const char* ce = std::getenv("FGB_SEARCH_CUCKOO");
+                const char* te0 = std::getenv("FGB_SEARCH_TIMING");  // (the timing variant is per-path dispatch)
+                if (pl.mode == approx::kModeHash && !(ce && ce[0] == '0') && !(te0 && te0[0] == '1')) {
+                    pl.mode = approx::kModeCuckoo;
+                    auto ck_cap = [](uint32_t nnz) {
+                        uint32_t c = 16;
+                        while (c < 4 * nnz) c <<= 1;
+                        return c;
+                    };
+                    pl.cap[0] = ck_cap(up.max_lnnz);
+                    pl.cap[1] = ck_cap(up.max_snnz);
+                }
             }
             pl.beamcap = std::max(max_beam, 32u);
             pl.kcap = std::max(max_k, 1u);
@@ -1463,7 +1476,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                   pl.gpool_d = reinterpret_cast<double*>(1);  // (placeholders: smem sizing only)
                   pl.gpool_n = reinterpret_cast<uint32_t*>(1);
               }
-              if (plain_warp_smem(pl) > 0) {
+              for (int ck_pass = 0; ck_pass < 2 && plain_warp_smem(pl) > 0; ++ck_pass) {
                 const uint64_t slots = plain_slots(pl, nq, c.device);
                 if (gpool) {
                     W.gpool.ensure(slots * pl.beamcap * 12);
@@ -1509,6 +1522,22 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                 launch_search_plain(pl, nq, c.device, s);
                 FGB_CUDA(cudaEventRecord(ix->ev1, s));
                 ht.mark("plain kernel");
+                if (pl.mode == approx::kModeCuckoo) {
+                    // a query without a cuckoo table (r_err 4; practically
+                    // never at <= 1/4 load): the batch runs again with hash lookups
+                    std::vector<uint32_t> h_err(nq);
+                    r_err.download(h_err.data(), nq, s);
+                    FGB_CUDA(cudaStreamSynchronize(s));
+                    if (std::any_of(h_err.begin(), h_err.end(), [](uint32_t e) { return e == 4; })) {
+                        pl.mode = approx::kModeHash;
+                        pl.cap[0] = hash_capacity(up.max_lnnz);
+                        pl.cap[1] = hash_capacity(up.max_snnz);
+                        pl.gpool_d = gpool ? reinterpret_cast<double*>(1) : nullptr;
+                        pl.gpool_n = gpool ? reinterpret_cast<uint32_t*>(1) : nullptr;
+                        FGB_CUDA(cudaMemsetAsync(io.work.get(), 0, sizeof(unsigned int), s));
+                        continue;
+                    }
+                }
                 if (pl.timing || pl.stats) {
                     unsigned long long t[kPlainPhCount] = {}, st[2] = {};
                     if (pl.timing) timing.download(t, kPlainPhCount, s);

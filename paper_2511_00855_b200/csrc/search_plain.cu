@@ -68,8 +68,9 @@ __device__ __forceinline__ PlainMem carve(unsigned char* base, const PlainLaunch
         return p;
     };
     m.qd = reinterpret_cast<float*>(take(a.c.dstride * 4));
-    m.path[0] = take(path_bytes(a.vocab[0], a.cap[0]));
-    m.path[1] = take(path_bytes(a.vocab[1], a.cap[1]));
+    const bool ck = a.mode == approx::kModeCuckoo;
+    m.path[0] = take(path_bytes(a.vocab[0], a.cap[0], ck));
+    m.path[1] = take(path_bytes(a.vocab[1], a.cap[1], ck));
     m.cand_d = a.gpool_d ? a.gpool_d + slot * a.beamcap : reinterpret_cast<double*>(take(a.beamcap * 8));
     m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
     m.cand_n = a.gpool_n ? a.gpool_n + slot * a.beamcap : reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
@@ -131,9 +132,18 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
             Q.qd = wd != 0.0f ? w.qd : nullptr;
             if (!Q.qd) qd2 = 0.0;
         }
-        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 0, w.path[0], Q.p[0], lane);
-        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 1, w.path[1], Q.p[1], lane);
+        constexpr bool kCk = kMode == approx::kModeCuckoo;
+        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 0, w.path[0], Q.p[0], lane, kCk);
+        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 1, w.path[1], Q.p[1], lane, kCk);
         __syncwarp();
+        if (kCk && (a.prefetch & 0x100) && (qi & 1) == 0) Q.p[0].hm1 = Q.p[1].hm1 = 0;  // test hook: forced failure
+        if (kCk && ((Q.p[0].on && !Q.p[0].hm1) || (Q.p[1].on && !Q.p[1].hm1))) {
+            if (lane == 0) {  // no cuckoo table: the host re-runs the batch with hash lookups
+                a.r_count[qi] = 0;
+                a.r_err[qi] = 4;
+            }
+            continue;
+        }
         // |weighted dense query| (screening) and |weighted query| over all paths (error bound)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -247,7 +257,9 @@ __global__ void __launch_bounds__(32, kMinWarps) search_plain_kernel(PlainLaunch
                 const float* pval = learned ? c.l_val : c.s_val;
                 const uint32_t off4 = learned ? mt.x : mt.y, pnnz = learned ? (mt.z & 0xFFFFu) : (mt.z >> 16);
                 double r;
-                if constexpr (kMode == approx::kModeBitmap)
+                if constexpr (kMode == approx::kModeCuckoo)
+                    r = sparse_group<approx::kLookCuckoo>(pidx, pval, P, off4, pnnz, lane, F);
+                else if constexpr (kMode == approx::kModeBitmap)
                     r = sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F);
                 else if constexpr (kMode == approx::kModeHash)
                     r = sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
@@ -433,6 +445,7 @@ template <int NQ4>
 void launch_t(const PlainLaunch& a, uint64_t blocks, size_t smem, cudaStream_t s) {
     switch (a.mode) {
         case approx::kModeHash: launch_m<NQ4, approx::kModeHash>(a, blocks, smem, s); break;
+        case approx::kModeCuckoo: launch_m<NQ4, approx::kModeCuckoo>(a, blocks, smem, s); break;
         default: launch_m<NQ4, approx::kModeMixed>(a, blocks, smem, s); break;
     }
 }
@@ -448,6 +461,7 @@ template <int NQ4>
 const void* kernel_ptr(int mode) {
     switch (mode) {
         case approx::kModeHash: return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false, approx::kModeHash>);
+        case approx::kModeCuckoo: return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false, approx::kModeCuckoo>);
         default: return reinterpret_cast<const void*>(search_plain_kernel<NQ4, false, approx::kModeMixed>);
     }
 }
@@ -468,8 +482,9 @@ const void* kernel_for(int v, int mode) {
 
 size_t plain_warp_smem(const PlainLaunch& a) {
     if (nq4_of(a) == 0) return 0;  // dense rows wider than 1,024 floats: general kernel
-    const size_t b = al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0])) +
-                     al16(path_bytes(a.vocab[1], a.cap[1])) + (a.gpool_d ? 0 : al16(a.beamcap * 8)) + al16(a.kcap * 8) +
+    const bool ck = a.mode == approx::kModeCuckoo;
+    const size_t b = al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0], ck)) +
+                     al16(path_bytes(a.vocab[1], a.cap[1], ck)) + (a.gpool_d ? 0 : al16(a.beamcap * 8)) + al16(a.kcap * 8) +
                      (a.gpool_n ? 0 : al16(a.beamcap * 4)) + al16(a.kcap * 4) + al16(32 * 4);
     return b <= 227 * 1024 ? b : 0;
 }

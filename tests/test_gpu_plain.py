@@ -167,3 +167,24 @@ def test_plain_hbm_cand_pool_identical(c2_small, ref, monkeypatch):
         q = synth.synth_queries(p, 32, beam_width=beam)
         same(fg.batch_query(gix, q, entry_count=64), ref.batch_query(rix, q, entry_count=64))
         assert gix.last_search_kernel() == "search_plain_kernel"
+
+
+@pytest.mark.parametrize("variant", ["cuckoo", "hash", "cuckoo-fallback"])
+def test_plain_hash_vocab_lookup_variants(ref, monkeypatch, variant):
+    """Hash-vocabulary batches (statistical vocab 831,592) run two-choice
+    cuckoo tables by default; the filter + hash layout (FGB_SEARCH_CUCKOO=0)
+    and the fallback after a failed cuckoo build (test hook: half the queries
+    fail, the batch re-runs with hash lookups) give the same results."""
+    if variant == "hash":
+        monkeypatch.setenv("FGB_SEARCH_CUCKOO", "0")
+    if variant == "cuckoo-fallback":
+        monkeypatch.setenv("FGB_SEARCH_PREFETCH", str(5 | 0x100))
+    p = A.synth_params(docs=3000, dense_dim=96, learned_vocab=30522, learned_nnz=60, statistical_vocab=831592,
+                       statistical_nnz=40, seed=12)
+    c, kg, _ = synth.generate_corpus(p, 0)
+    dc = fg.DeviceCorpus(c)
+    gix = fg.build_hybrid_index(dc, kg, degree=16, knn_k=32, seed=42)
+    rix = ref.index_create(ref.store(c, kg), gix.export(), 32)
+    q = synth.synth_queries(p, 80, beam_width=96)
+    same(fg.batch_query(gix, q, entry_count=64), ref.batch_query(rix, q, entry_count=64))
+    assert gix.last_search_kernel() == "search_plain_kernel"
