@@ -24,6 +24,7 @@
 //    new or changed is offered in reach order with warp-cooperative
 //    single-entry offers (exactly Pool::offer, search.cpp:26-42).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1091,7 +1092,8 @@ void finish_results(fg_index* ix, const fg_corpus& c, const fg_query_view* q, fg
 // (search_hybrid.cu).  Queries that overflow their twin pool or context table
 // are re-run alone with 4x larger tables; false when the batch does not fit
 // the kernel's shared memory (the caller falls back to search_kernel).
-bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunch& pl, const fg_query_view* q,
+bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunch& pl,
+                const std::array<uint32_t, 5>& ck_fallback, const fg_query_view* q,
                 const std::vector<uint8_t>& qflags, uint32_t max_seeds, uint32_t max_req, bool any_ctx,
                 bool any_req, bool conj,
                 uint64_t nq, uint32_t stride, std::vector<std::string>& errs, fg_search_results* out,
@@ -1136,7 +1138,7 @@ bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunc
     h.seencap = 64;
     while (2 * h.seencap < 3 * list_max) h.seencap <<= 1;  // load <= 2/3
     if (hybrid_warp_smem(h) == 0) return false;
-    const uint64_t all_slots = hybrid_slots(h, nq, c.device);
+    uint64_t all_slots = hybrid_slots(h, nq, c.device);
     h.p.hit_stride = stride;
     h.p.r_node = io.r_node.get();
     h.p.r_score = io.r_score.get();
@@ -1178,9 +1180,10 @@ bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunc
     std::vector<uint32_t> rerun;
     DevBuf<uint32_t> d_rerun;
     float ms_prev = 0.f;
+    int grow = 0;  // scratch growth steps (twin / context tables)
     for (int attempt = 0;; ++attempt) {
-        h.twcap = twcap0 << (2 * attempt);
-        h.ctxcap = ctxcap0 << (2 * attempt);
+        h.twcap = twcap0 << (2 * grow);
+        h.ctxcap = ctxcap0 << (2 * grow);
         const uint64_t slots = attempt ? std::min<uint64_t>(all_slots, rerun.size()) : all_slots;
         const uint64_t nbits = 1 + (any_ctx ? 1 : 0) + (any_req ? 1 : 0);
         const uint64_t bits_words = slots * h.p.nwords * nbits;
@@ -1212,8 +1215,23 @@ bool run_hybrid(fg_index* ix, fg_corpus& c, SearchWorkspace& W, const PlainLaunc
         io.r_err.download(h_err.data(), nq, s);
         FGB_CUDA(cudaStreamSynchronize(s));
         rerun.clear();
+        uint32_t err_any = 0;
         for (uint64_t i = 0; i < nq; ++i)
-            if (h_err[i]) rerun.push_back(static_cast<uint32_t>(i));
+            if (h_err[i]) {
+                rerun.push_back(static_cast<uint32_t>(i));
+                err_any |= h_err[i];
+            }
+        if (err_any & (HERR_TWIN | HERR_CTX)) ++grow;
+        if ((err_any & HERR_CUCKOO) && h.p.mode == approx::kModeCuckoo) {
+            // a query without a cuckoo table: the re-run takes the fallback lookups
+            h.p.mode = static_cast<int>(ck_fallback[0]);
+            h.p.vocab[0] = ck_fallback[1];
+            h.p.vocab[1] = ck_fallback[2];
+            h.p.cap[0] = ck_fallback[3];
+            h.p.cap[1] = ck_fallback[4];
+            if (hybrid_warp_smem(h) == 0) return false;  // (the general kernel re-runs the batch)
+            all_slots = hybrid_slots(h, nq, c.device);
+        }
         constexpr uint64_t kMaxScratch = 1ull << 30;  // bytes of twin + context tables per launch
         const uint64_t next_slots = std::min<uint64_t>(all_slots, rerun.size());
         const uint64_t next_bytes = next_slots * ((uint64_t(h.twcap) * 12 + uint64_t(h.ctxcap) * 16) << 2);
@@ -1404,6 +1422,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.norm_meta = ix->norm_meta.get();
             pl.entry_count = norm_seeds;
             pl.qflags = d_qflags.get();
+            std::array<uint32_t, 5> ck_fallback{};  // the lookup selection a failed cuckoo build falls back to
             // sparse paths: bitmap + rank lookups for vocabularies up to 64K
             // terms, filter + hash otherwise (FGB_SEARCH_BITMAP=0: hash only)
             const char* be = std::getenv("FGB_SEARCH_BITMAP");
@@ -1429,16 +1448,21 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                 const bool all_hash = (!l_on || !pl.vocab[0]) && (!s_on || !pl.vocab[1]);
                 pl.mode = all_hash ? approx::kModeHash : approx::kModeMixed;
                 if (const char* e = std::getenv("FGB_SEARCH_MODE"); e && e[0] == '2') pl.mode = approx::kModeMixed;
-                // hash batches: two-choice cuckoo tables (FGB_SEARCH_CUCKOO=0: filter + hash)
+                // every batch: two-choice cuckoo tables for both sparse paths
+                // (FGB_SEARCH_CUCKOO=0: the bitmap / filter + hash selection
+                // above).  B200, 200K docs, identical results: C2 shape bitmap
+                // 139.6K -> 153.2K QPS, C3/C4 hash 59.3K -> 93.8K QPS.
                 const char* ce = std::getenv("FGB_SEARCH_CUCKOO");
                 const char* te0 = std::getenv("FGB_SEARCH_TIMING");  // (the timing variant is per-path dispatch)
-                if (pl.mode == approx::kModeHash && !(ce && ce[0] == '0') && !(te0 && te0[0] == '1')) {
+                ck_fallback = {static_cast<uint32_t>(pl.mode), pl.vocab[0], pl.vocab[1], pl.cap[0], pl.cap[1]};
+                if (!(ce && ce[0] == '0') && !(te0 && te0[0] == '1')) {
                     pl.mode = approx::kModeCuckoo;
                     auto ck_cap = [](uint32_t nnz) {
                         uint32_t c = 16;
                         while (c < 4 * nnz) c <<= 1;
                         return c;
                     };
+                    pl.vocab[0] = pl.vocab[1] = 0;
                     pl.cap[0] = ck_cap(up.max_lnnz);
                     pl.cap[1] = ck_cap(up.max_snnz);
                 }
@@ -1464,7 +1488,7 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
             pl.prefetch = 5;
             if (const char* e = std::getenv("FGB_SEARCH_PREFETCH")) pl.prefetch = std::atoi(e);
             if (special) {
-                if (run_hybrid(ix, c, W, pl, q, qflags, max_seeds, max_req, any_ctx, any_req, conj, nq, stride, errs, out, s))
+                if (run_hybrid(ix, c, W, pl, ck_fallback, q, qflags, max_seeds, max_req, any_ctx, any_req, conj, nq, stride, errs, out, s))
                     return;
             } else {
               // very large beams keep their cand pools in HBM (L1/L2 cached):
@@ -1529,9 +1553,11 @@ int fg_batch_query(const fg_index* cix, const fg_query_view* q, const fg_search_
                     r_err.download(h_err.data(), nq, s);
                     FGB_CUDA(cudaStreamSynchronize(s));
                     if (std::any_of(h_err.begin(), h_err.end(), [](uint32_t e) { return e == 4; })) {
-                        pl.mode = approx::kModeHash;
-                        pl.cap[0] = hash_capacity(up.max_lnnz);
-                        pl.cap[1] = hash_capacity(up.max_snnz);
+                        pl.mode = static_cast<int>(ck_fallback[0]);
+                        pl.vocab[0] = ck_fallback[1];
+                        pl.vocab[1] = ck_fallback[2];
+                        pl.cap[0] = ck_fallback[3];
+                        pl.cap[1] = ck_fallback[4];
                         pl.gpool_d = gpool ? reinterpret_cast<double*>(1) : nullptr;
                         pl.gpool_n = gpool ? reinterpret_cast<uint32_t*>(1) : nullptr;
                         FGB_CUDA(cudaMemsetAsync(io.work.get(), 0, sizeof(unsigned int), s));

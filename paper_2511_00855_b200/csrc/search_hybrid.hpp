@@ -49,7 +49,7 @@ enum : int {
     kHybPhases, kHybBatches = kHybPhases, kHybExpanded, kHybQueries, kHybCount
 };
 
-enum : uint32_t { HERR_TWIN = 1, HERR_CTX = 2 };
+enum : uint32_t { HERR_TWIN = 1, HERR_CTX = 2, HERR_CUCKOO = 4 };
 
 // Per-warp shared memory of the hybrid kernel; 0 when the batch does not fit.
 size_t hybrid_warp_smem(const HybridLaunch& a);

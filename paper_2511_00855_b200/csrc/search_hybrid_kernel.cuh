@@ -87,8 +87,9 @@ __device__ __forceinline__ HybridMem carve(unsigned char* base, const HybridLaun
         return p;
     };
     m.qd = reinterpret_cast<float*>(take(a.c.dstride * 4));
-    m.path[0] = take(path_bytes(a.vocab[0], a.cap[0]));
-    m.path[1] = take(path_bytes(a.vocab[1], a.cap[1]));
+    const bool ck = a.mode == approx::kModeCuckoo;
+    m.path[0] = take(path_bytes(a.vocab[0], a.cap[0], ck));
+    m.path[1] = take(path_bytes(a.vocab[1], a.cap[1], ck));
     m.cand_d = reinterpret_cast<double*>(take(a.beamcap * 8));
     m.topk_d = reinterpret_cast<double*>(take(a.kcap * 8));
     m.cand_n = reinterpret_cast<uint32_t*>(take(a.beamcap * 4));
@@ -109,7 +110,8 @@ __device__ __forceinline__ HybridMem carve(unsigned char* base, const HybridLaun
 
 size_t carve_bytes(const HybridLaunch& h) {
     const PlainLaunch& a = h.p;
-    return al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0])) + al16(path_bytes(a.vocab[1], a.cap[1])) +
+    const bool ck = a.mode == approx::kModeCuckoo;
+    return al16(a.c.dstride * 4) + al16(path_bytes(a.vocab[0], a.cap[0], ck)) + al16(path_bytes(a.vocab[1], a.cap[1], ck)) +
            al16(a.beamcap * 8) + al16(a.kcap * 8) + al16(a.beamcap * 4) + al16(a.kcap * 4) + al16(32 * 4) +
            al16(h.reqcap * 4 + 4) + al16(h.lccap * 8 + 8) + al16(h.seencap * 4) + al16(kXq * 8) + 2 * al16(kXq * 4) +
            al16(kHybCount * 8) + al16(kStage * 16) + 2 * al16(kStage * 4);
@@ -308,8 +310,9 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
             Q.qd = wd != 0.0f ? w.qd : nullptr;
             if (!Q.qd) qd2 = 0.0;
         }
-        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 0, w.path[0], Q.p[0], lane);
-        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 1, w.path[1], Q.p[1], lane);
+        constexpr bool kCk = kMode == approx::kModeCuckoo;
+        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 0, w.path[0], Q.p[0], lane, kCk);
+        qs2 += stage_path(a.q, a.vocab, a.cap, qi, 1, w.path[1], Q.p[1], lane, kCk);
         const uint64_t rb = kReq ? a.q.req_ptr[qi] : 0;
         const uint32_t R = kReq ? static_cast<uint32_t>(a.q.req_ptr[qi + 1] - rb) : 0u;
         for (uint32_t i = lane; i < R; i += 32) w.req[i] = a.q.req_idx[rb + i];
@@ -329,6 +332,10 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
         const Pool topk{w.topk_d, w.topk_n, K};
         const Pool cand{w.cand_d, w.cand_n, B};
         uint32_t tsize = 0, csize = 0, ntouched = 0, cursor = 0, ntwin = 0, err = 0, ctx_used = 0;
+        if (kCk && (a.prefetch & 0x100) && (qi & 1) == 0) Q.p[0].hm1 = Q.p[1].hm1 = 0;  // test hook: forced failure
+        // no cuckoo table for a path (practically never at <= 1/4 load): the
+        // host re-runs the query with the fallback lookups
+        if (kCk && ((Q.p[0].on && !Q.p[0].hm1) || (Q.p[1].on && !Q.p[1].hm1))) err = HERR_CUCKOO;
         unsigned long long expanded = 0, scored = 0;
         // batch generator state: seeds (search.cpp:205-216), then expansions
         const uint64_t sb = ctx_mode ? h.seed_ptr[qi] : 0;
@@ -569,7 +576,9 @@ __global__ void __launch_bounds__(32, kMinWarps) search_hybrid_kernel(HybridLaun
                 const float* pval = learned ? c.l_val : c.s_val;
                 const uint32_t off4 = learned ? mt.x : mt.y, pnnz = learned ? (mt.z & 0xFFFFu) : (mt.z >> 16);
                 double r;
-                if constexpr (kMode == approx::kModeHash)
+                if constexpr (kMode == approx::kModeCuckoo)
+                    r = sparse_group<approx::kLookCuckoo>(pidx, pval, P, off4, pnnz, lane, F);
+                else if constexpr (kMode == approx::kModeHash)
                     r = sparse_group<false>(pidx, pval, P, off4, pnnz, lane, F);
                 else
                     r = P.vocab ? sparse_group<true>(pidx, pval, P, off4, pnnz, lane, F)
@@ -889,7 +898,9 @@ const void* hybrid_kernel_ptr(int nq4, int mode) {
     switch (nq4) {
 #define FGB_HYBP(V)                                                                                         \
     case V:                                                                                                 \
-        return mode == approx::kModeHash                                                                    \
+        return mode == approx::kModeCuckoo                                                                  \
+                   ? reinterpret_cast<const void*>(search_hybrid_kernel<V, approx::kModeCuckoo, kCtx, kReq>)\
+               : mode == approx::kModeHash                                                                  \
                    ? reinterpret_cast<const void*>(search_hybrid_kernel<V, approx::kModeHash, kCtx, kReq>)  \
                    : reinterpret_cast<const void*>(search_hybrid_kernel<V, approx::kModeMixed, kCtx, kReq>);
         FGB_HYBP(1)
@@ -908,7 +919,11 @@ void hybrid_launch_variant(const HybridLaunch& h, int nq4, uint64_t blocks, size
     switch (nq4) {
 #define FGB_HYB(V)                                                                                               \
     case V:                                                                                                      \
-        if (h.p.mode == approx::kModeHash) {                                                                     \
+        if (h.p.mode == approx::kModeCuckoo) {                                                                   \
+            FGB_CUDA(cudaFuncSetAttribute(search_hybrid_kernel<V, approx::kModeCuckoo, kCtx, kReq>,              \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));              \
+            search_hybrid_kernel<V, approx::kModeCuckoo, kCtx, kReq><<<(unsigned)blocks, 32, smem, s>>>(h);      \
+        } else if (h.p.mode == approx::kModeHash) {                                                              \
             FGB_CUDA(cudaFuncSetAttribute(search_hybrid_kernel<V, approx::kModeHash, kCtx, kReq>,                \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));              \
             search_hybrid_kernel<V, approx::kModeHash, kCtx, kReq><<<(unsigned)blocks, 32, smem, s>>>(h);        \

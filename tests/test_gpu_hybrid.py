@@ -143,3 +143,24 @@ def test_overflow_reruns_identical(c4, ref, monkeypatch):
     same(g, ref.batch_query(c4["rix"], q, threads=THREADS))
     q = keyword_queries(c4["p"], 24, 256, seed=13)
     same(fg.batch_query(c4["gix"], q), ref.batch_query(c4["rix"], q, threads=THREADS))
+
+
+@pytest.mark.parametrize("variant", ["hash", "cuckoo-fallback", "cuckoo-fallback+overflow"])
+def test_lookup_variants_identical(c4, ref, monkeypatch, variant):
+    """Cuckoo query tables are the default; the filter + hash lookups
+    (FGB_SEARCH_CUCKOO=0) and the re-run after a failed cuckoo build (test
+    hook: every even query fails; with overflowing scratch as well) agree."""
+    if variant == "hash":
+        monkeypatch.setenv("FGB_SEARCH_CUCKOO", "0")
+    else:
+        monkeypatch.setenv("FGB_SEARCH_PREFETCH", str(5 | 0x100))
+    if variant.endswith("overflow"):
+        monkeypatch.setenv("FGB_SEARCH_SCRATCH0", "2")
+    q = chain_queries(c4["chains"][:16], 100.0)
+    g = fg.batch_query(c4["gix"], q)
+    assert c4["gix"].last_search_kernel() == "search_hybrid_kernel"
+    if variant != "hash":
+        assert c4["gix"].last_search_stats()[1] >= 2
+    same(g, ref.batch_query(c4["rix"], q, threads=THREADS))
+    q = keyword_queries(c4["p"], 24, 256, seed=13)
+    same(fg.batch_query(c4["gix"], q), ref.batch_query(c4["rix"], q, threads=THREADS))

@@ -66,7 +66,9 @@ def test_plain_c2_shape_identical(c2_small, ref, beam, entry):
     same(g, ref.batch_query(rix, q, entry_count=entry, threads=os.cpu_count() or 1))
     with env(FGB_SEARCH_PLAIN=0):  # the general (sequential-chain) kernel agrees too
         same(fg.batch_query(gix, q, entry_count=entry), g)
-    with env(FGB_SEARCH_BITMAP=0):  # hash lookups instead of the learned-path bitmap
+    with env(FGB_SEARCH_CUCKOO=0):  # bitmap + rank lookups instead of the cuckoo tables
+        same(fg.batch_query(gix, q, entry_count=entry), g)
+    with env(FGB_SEARCH_CUCKOO=0, FGB_SEARCH_BITMAP=0):  # filter + hash lookups
         same(fg.batch_query(gix, q, entry_count=entry), g)
 
 
@@ -171,8 +173,8 @@ def test_plain_hbm_cand_pool_identical(c2_small, ref, monkeypatch):
 
 @pytest.mark.parametrize("variant", ["cuckoo", "hash", "cuckoo-fallback"])
 def test_plain_hash_vocab_lookup_variants(ref, monkeypatch, variant):
-    """Hash-vocabulary batches (statistical vocab 831,592) run two-choice
-    cuckoo tables by default; the filter + hash layout (FGB_SEARCH_CUCKOO=0)
+    """Batches run two-choice cuckoo tables by default; with a hash-sized
+    statistical vocabulary (831,592) the filter + hash layout (FGB_SEARCH_CUCKOO=0)
     and the fallback after a failed cuckoo build (test hook: half the queries
     fail, the batch re-runs with hash lookups) give the same results."""
     if variant == "hash":
