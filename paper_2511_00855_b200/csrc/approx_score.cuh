@@ -96,6 +96,54 @@ __device__ __forceinline__ float q_lookup_m(const PathQ& P, uint32_t t, bool& fo
         return q_lookup(P, t, found);
 }
 
+// Odd multipliers of the cuckoo tables, tried in order until every query
+// term has a slot (a table at <= 1/4 load practically never needs the second).
+__device__ __constant__ const uint32_t kCuckooMul[8][2] = {
+    {0x9E3779B1u, 0x85EBCA77u}, {0xC2B2AE3Du, 0x27D4EB2Fu}, {0x165667B1u, 0xD3A2646Du}, {0xFD7046C5u, 0xB55A4F09u},
+    {0x2545F491u, 0x4F1BBCDDu}, {0x68E31DA5u, 0x1B873593u}, {0xCC9E2D51u, 0x7FEB352Du}, {0x846CA68Bu, 0xE6546B65u}};
+
+// Fills a two-choice cuckoo table of `cap` slots (a power of two, >= 4 nt)
+// with the nt pairs tk/tv (staged in shared memory; warp-cooperative, lane 0
+// inserts — a table at <= 1/4 load takes a few kicks at most).  Sets P.hm1/
+// P.hm2 (P.hshift must be set); P.hm1 = 0 when no multiplier pair worked.
+__device__ inline void cuckoo_fill(PathQ& P, uint32_t* keys, float* vals, const uint32_t* tk, const float* tv,
+                                   uint32_t nt, uint32_t cap, uint32_t lane) {
+    bool ok = false;
+    for (int seed = 0; seed < 8 && !ok; ++seed) {
+        const uint32_t m1 = kCuckooMul[seed][0], m2 = kCuckooMul[seed][1], sh = P.hshift;
+        for (uint32_t j = lane; j < cap; j += 32) keys[j] = kEmpty;
+        __syncwarp();
+        uint32_t good = 1;
+        if (lane == 0) {
+            for (uint32_t j = 0; j < nt && good; ++j) {
+                uint32_t key = tk[j];
+                float val = tv[j];
+                uint32_t pos = (key * m1) >> sh;
+                good = 0;
+                for (uint32_t kick = 0; kick < 4 * nt + 16; ++kick) {
+                    const uint32_t old = keys[pos];
+                    const float oldv = vals[pos];
+                    keys[pos] = key;
+                    vals[pos] = val;
+                    if (old == kEmpty) {
+                        good = 1;
+                        break;
+                    }
+                    key = old;
+                    val = oldv;
+                    const uint32_t p1 = (key * m1) >> sh;
+                    pos = pos == p1 ? (key * m2) >> sh : p1;
+                }
+            }
+        }
+        ok = __shfl_sync(kFull, good, 0) != 0;
+        P.hm1 = m1;
+        P.hm2 = m2;
+        __syncwarp();
+    }
+    if (!ok) P.hm1 = 0;  // no table found: the caller fails the query (or node)
+}
+
 // ------------------------------------------------------------ scoring
 // The query terms among 4 postings.  kF32 = false: exact fp64 products summed
 // in fp64 (each product predicated on the lookup hit).  kF32 = true: fp32

@@ -139,7 +139,15 @@ struct PassArgs {
     unsigned int* overflow;  // pool overflow counter (0 after a correct pass)
     const uint32_t* order;   // CTA b processes node order[lo + b] (graph locality); nullptr: lo + b
     unsigned long long* counts;  // [0] candidates scored (sum of S_u), [1] dense rows read
+    uint32_t ck_cap[2];          // cuckoo variant: table slots per path (power of two >= 4 max nnz)
+    unsigned int* ck_fail;       // cuckoo variant: nodes without a table (the host re-runs the pass)
+    uint32_t ck_test_fail;       // test hook (FGB_KNN_CUCKOO=2): nodes u % 7 == 3 fail their tables
 };
+
+// Shared-memory bytes of one path's cuckoo table: keys, values, staged row.
+__host__ __device__ __forceinline__ size_t ck_bytes(uint32_t cap) {
+    return (static_cast<size_t>(cap) * 8 + static_cast<size_t>(cap / 4) * 8 + 15) & ~size_t(15);
+}
 
 enum : int {
     kKnPhInit = 0, kKnPhPool, kKnPhScore, kKnPhMerge, kKnPhExact, kKnPhFinal,  // cycles (thread 0)
@@ -396,7 +404,7 @@ __device__ void merge_certify_sorted(const PassArgs& a, const SmemQuery& sq, uin
 // rejected when certified worse than the running k-th entry; only the rest
 // get the exact chain.  NQ4 == 0 (dense rows > 1,024 floats): exact chains,
 // thread per candidate.
-template <int NQ4>
+template <int NQ4, bool kCk>
 __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t k = a.k;
@@ -462,10 +470,57 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
             P[p].filt = p == 0 ? sq.lfilt : sq.sfilt;
             P[p].mask = p == 0 ? sq.lmask : sq.smask;
         }
-        // learned path of u as a bitmap + rank structure (branch-free lookups)
+        if constexpr (kCk) {
+            // u's sparse rows as two-choice cuckoo tables (exactly two probes
+            // per lookup): warp 0 builds, the others read the multipliers
+            __shared__ uint32_t ck_hm[2][2];
+            unsigned char* ckm = reinterpret_cast<unsigned char*>(qd + a.c.dstride);
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const uint32_t cap = a.ck_cap[p];
+                uint32_t* ck = reinterpret_cast<uint32_t*>(ckm + (p ? ck_bytes(a.ck_cap[0]) : 0));
+                float* cv = reinterpret_cast<float*>(ck + cap);
+                P[p].vocab = 0;
+                P[p].keys = ck;
+                P[p].vals = cv;
+                P[p].mask = cap - 1;
+                P[p].hshift = 32u - static_cast<uint32_t>(__ffs(cap) - 1);
+                if (!cap) continue;  // (the learned path on its bitmap)
+                if (tid < 32 && P[p].on) {
+                    uint32_t* tk = reinterpret_cast<uint32_t*>(cv + cap);
+                    float* tv = reinterpret_cast<float*>(tk + cap / 4);
+                    const uint64_t ro = p ? a.c.s_off[u] : a.c.l_off[u];
+                    const uint32_t rn = p ? a.c.s_nnz[u] : a.c.l_nnz[u];
+                    for (uint32_t j = tid; j < rn; j += 32) {
+                        tk[j] = (p ? a.c.s_idx : a.c.l_idx)[ro + j];
+                        tv[j] = (p ? a.c.s_val : a.c.l_val)[ro + j];
+                    }
+                    approx::cuckoo_fill(P[p], ck, cv, tk, tv, rn, cap, tid);
+                    if (tid == 0) {
+                        ck_hm[p][0] = P[p].hm1;
+                        ck_hm[p][1] = P[p].hm2;
+                    }
+                }
+            }
+            __syncthreads();
+            bool bad = a.ck_test_fail && u % 7 == 3;
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+                if (P[p].on && a.ck_cap[p]) {
+                    P[p].hm1 = ck_hm[p][0];
+                    P[p].hm2 = ck_hm[p][1];
+                    bad |= P[p].hm1 == 0;
+                }
+            if (bad) {  // (uniform over the CTA) nothing of u is written; the host re-runs the pass
+                if (tid == 0) atomicAdd(a.ck_fail, 1u);
+                return;
+            }
+        }
         if (a.l_vocab && P[0].on) {
+            // learned path of u as a bitmap + rank structure (branch-free lookups)
             const uint32_t W = approx::bitmap_words(a.l_vocab);
-            uint32_t* bm = reinterpret_cast<uint32_t*>(qd + a.c.dstride);
+            uint32_t* bm = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(qd + a.c.dstride) +
+                                                       (kCk ? ck_bytes(a.ck_cap[0]) + ck_bytes(a.ck_cap[1]) : 0));
             uint16_t* pre = reinterpret_cast<uint16_t*>(bm + ((W + 3) & ~3u));
             float* qv = reinterpret_cast<float*>(pre + ((W + 7) & ~7u));
             const uint64_t lo = a.c.l_off[u];
@@ -634,10 +689,21 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
                     }
                 }
                 double L = 0.0, S = 0.0;
-                if (P[0].on)
-                    L = P[0].vocab ? approx::sparse_group<true, true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F)
-                                   : approx::sparse_group<false, true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
-                if (P[1].on) S = approx::sparse_group<false, true>(a.c.s_idx, a.c.s_val, P[1], mt.y, mt.z >> 16, lane, F);
+                if constexpr (kCk) {  // learned: bitmap or cuckoo; statistical: cuckoo
+                    if (P[0].on)
+                        L = P[0].vocab ? approx::sparse_group<true, true>(a.c.l_idx, a.c.l_val, P[0], mt.x,
+                                                                          mt.z & 0xFFFFu, lane, F)
+                                       : approx::sparse_group<approx::kLookCuckoo, true>(a.c.l_idx, a.c.l_val, P[0],
+                                                                                         mt.x, mt.z & 0xFFFFu, lane, F);
+                    if (P[1].on)
+                        S = approx::sparse_group<approx::kLookCuckoo, true>(a.c.s_idx, a.c.s_val, P[1], mt.y,
+                                                                            mt.z >> 16, lane, F);
+                } else {
+                    if (P[0].on)
+                        L = P[0].vocab ? approx::sparse_group<true, true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F)
+                                       : approx::sparse_group<false, true>(a.c.l_idx, a.c.l_val, P[0], mt.x, mt.z & 0xFFFFu, lane, F);
+                    if (P[1].on) S = approx::sparse_group<false, true>(a.c.s_idx, a.c.s_val, P[1], mt.y, mt.z >> 16, lane, F);
+                }
                 // screening: the exact score is <= the bound (+ the approximation error)
                 bool keep = mine && !(score_upper_bound(unorm, (double)__uint_as_float(mt.w), L, S) + 2.0 * eps < tau_lo);
                 const uint32_t km = __ballot_sync(approx::kFull, keep);
@@ -832,12 +898,13 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
 }
 
 size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap,
-                 uint32_t l_vocab) {
+                 uint32_t l_vocab, const uint32_t* ck_cap) {
     size_t b = (doc_stage_bytes(dstride, lcap, scap) + 15) & ~size_t(15);
     b += static_cast<size_t>(pool_cap) * 4 + 2 * (pool_cap / 32) * 4;
     b += (2 * k + kSCap) * 8 + (2 * k + kSCap) * 4;
     b += 2 * k + 3 * k + 2 * kSCap + 16;                  // new / exact / mark flags, alignment
     b += static_cast<size_t>(dstride) * 4;                // fp32 dense row of u
+    if (ck_cap) b += ck_bytes(ck_cap[0]) + ck_bytes(ck_cap[1]);  // u's cuckoo tables
     if (l_vocab) {                                        // u's learned bitmap, prefix, values
         const size_t W = approx::bitmap_words(l_vocab);
         b += ((W + 3) & ~size_t(3)) * 4 + ((W + 7) & ~size_t(7)) * 2 + static_cast<size_t>(lcap) * 4;
@@ -859,12 +926,12 @@ uint32_t pool_slots(double items) {
 // overflows fails the pass loudly).
 constexpr size_t kSmemTwo = 113 * 1024;
 void pool_plan(uint64_t n, uint32_t k, uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t l_vocab,
-               uint32_t& cap, uint32_t& nparts) {
+               const uint32_t* ck_cap, uint32_t& cap, uint32_t& nparts) {
     const double worst = static_cast<double>(std::min<uint64_t>(n, 4ull * k * k + k));
     for (nparts = 1;; nparts <<= 1) {
         const double per = nparts == 1 ? worst : worst / nparts + 4.0 * std::sqrt(worst / nparts) + 64.0;
         cap = pool_slots(per);
-        if (pass_smem(dstride, lcap, scap, k, cap, l_vocab) <= kSmemTwo || cap <= kPassThreads || nparts >= 64)
+        if (pass_smem(dstride, lcap, scap, k, cap, l_vocab, ck_cap) <= kSmemTwo || cap <= kPassThreads || nparts >= 64)
             return;
     }
 }
@@ -878,8 +945,16 @@ int pass_nq4(uint32_t dstride) {
 
 template <int NQ4>
 void launch_pass(const PassArgs& a, uint64_t blocks, size_t sm, cudaStream_t s) {
-    FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel<NQ4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    knn_pass_kernel<NQ4><<<(unsigned)blocks, kPassThreads, sm, s>>>(a);
+    if constexpr (NQ4 > 0) {
+        if (a.ck_cap[0] || a.ck_cap[1]) {
+            FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel<NQ4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sm));
+            knn_pass_kernel<NQ4, true><<<(unsigned)blocks, kPassThreads, sm, s>>>(a);
+            return;
+        }
+    }
+    FGB_CUDA(cudaFuncSetAttribute(knn_pass_kernel<NQ4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    knn_pass_kernel<NQ4, false><<<(unsigned)blocks, kPassThreads, sm, s>>>(a);
     FGB_LAUNCH("knn_pass_kernel");
 }
 
@@ -1023,46 +1098,75 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     }
     a.max_dnorm = c.max_dnorm * (1.0 + 1e-6);
     a.max_norm = std::sqrt(std::max(c.max_sqnorm, 0.0)) * (1.0 + 1e-9);
-    a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;
-    pool_plan(g.n, k, c.dstride, lcap, scap, a.l_vocab, a.pool_cap, a.nparts);
-    if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab) > 227 * 1024) {
-        a.l_vocab = 0;
-        pool_plan(g.n, k, c.dstride, lcap, scap, 0, a.pool_cap, a.nparts);
-    }
-    if (const char* e = std::getenv("FGB_KNN_PARTS")) {  // dev/test: force a part count (power of two)
-        const uint32_t v = static_cast<uint32_t>(std::atoi(e));
-        if (v >= 1 && (v & (v - 1)) == 0) {
-            a.nparts = v;
-            const double worst = static_cast<double>(std::min<uint64_t>(g.n, 4ull * k * k + k));
-            a.pool_cap = pool_slots(v == 1 ? worst : worst / v + 4.0 * std::sqrt(worst / v) + 64.0);
-        }
-    }
-    a.pshift = 32 - static_cast<uint32_t>(__builtin_ctz(a.nparts));
-    DevBuf<unsigned int> overflow(1);
-    overflow.zero(s);
-    a.overflow = overflow.get();
-    const size_t sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab);
-    if (sm > 227 * 1024)
-        throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
-                                            std::to_string(sm) + " B)");
     int nq4 = c.dc.meta ? pass_nq4(c.dstride) : 0;
     if (const char* e = std::getenv("FGB_KNN_EXACT"))  // dev: the exact-chain-only pass
         if (e[0] == '1') nq4 = 0;
-    const uint64_t blocks = hi - lo;
-    switch (nq4) {
-        case 1: launch_pass<1>(a, blocks, sm, s); break;
-        case 2: launch_pass<2>(a, blocks, sm, s); break;
-        case 3: launch_pass<3>(a, blocks, sm, s); break;
-        case 4: launch_pass<4>(a, blocks, sm, s); break;
-        case 6: launch_pass<6>(a, blocks, sm, s); break;
-        case 8: launch_pass<8>(a, blocks, sm, s); break;
-        default: launch_pass<0>(a, blocks, sm, s); break;
+    // u's sparse rows: two-choice cuckoo tables (FGB_KNN_CUCKOO=0: learned
+    // bitmap + filter/hash); a node without a table (practically never at
+    // <= 1/4 load) fails the cuckoo launch and the pass re-runs without
+    bool ck = nq4 > 0;
+    if (const char* e = std::getenv("FGB_KNN_CUCKOO"); e && e[0] == '0') ck = false;
+    if (const char* e = std::getenv("FGB_KNN_CUCKOO"); e && e[0] == '2') a.ck_test_fail = 1;
+    DevBuf<unsigned int> flags(2);  // [0] pool overflow, [1] nodes without a cuckoo table
+    DevBuf<unsigned long long> changed0;
+    if (ck) {
+        changed0.alloc(1);
+        FGB_CUDA(cudaMemcpyAsync(changed0.get(), d_changed, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
     }
-    {
-        unsigned int ov = 0;
-        overflow.download(&ov, 1, s);
+    const uint64_t blocks = hi - lo;
+    size_t sm = 0;
+    for (;;) {
+        auto ck_cap = [](uint32_t nnz) {
+            uint32_t v = 16;
+            while (v < 4 * nnz) v <<= 1;
+            return v;
+        };
+        // the learned path keeps its bitmap where the vocabulary allows (a
+        // bitmap beat the cuckoo table in this kernel: 1M C2 NN-Descent
+        // 12.25 s vs 12.84 s); hash-sized paths take cuckoo tables
+        a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;
+        a.ck_cap[0] = ck && !a.l_vocab && c.max_lnnz ? ck_cap(c.max_lnnz) : 0;
+        a.ck_cap[1] = ck && c.max_snnz ? ck_cap(c.max_snnz) : 0;
+        pool_plan(g.n, k, c.dstride, lcap, scap, a.l_vocab, a.ck_cap, a.pool_cap, a.nparts);
+        if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap) > 227 * 1024) {
+            a.l_vocab = 0;
+            a.ck_cap[0] = ck && c.max_lnnz ? ck_cap(c.max_lnnz) : 0;
+            pool_plan(g.n, k, c.dstride, lcap, scap, 0, a.ck_cap, a.pool_cap, a.nparts);
+        }
+        if (const char* e = std::getenv("FGB_KNN_PARTS")) {  // dev/test: force a part count (power of two)
+            const uint32_t v = static_cast<uint32_t>(std::atoi(e));
+            if (v >= 1 && (v & (v - 1)) == 0) {
+                a.nparts = v;
+                const double worst = static_cast<double>(std::min<uint64_t>(g.n, 4ull * k * k + k));
+                a.pool_cap = pool_slots(v == 1 ? worst : worst / v + 4.0 * std::sqrt(worst / v) + 64.0);
+            }
+        }
+        a.pshift = 32 - static_cast<uint32_t>(__builtin_ctz(a.nparts));
+        flags.zero(s);
+        a.overflow = flags.get();
+        a.ck_fail = flags.get() + 1;
+        sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap);
+        if (sm > 227 * 1024)
+            throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
+                                                std::to_string(sm) + " B)");
+        switch (nq4) {
+            case 1: launch_pass<1>(a, blocks, sm, s); break;
+            case 2: launch_pass<2>(a, blocks, sm, s); break;
+            case 3: launch_pass<3>(a, blocks, sm, s); break;
+            case 4: launch_pass<4>(a, blocks, sm, s); break;
+            case 6: launch_pass<6>(a, blocks, sm, s); break;
+            case 8: launch_pass<8>(a, blocks, sm, s); break;
+            default: launch_pass<0>(a, blocks, sm, s); break;
+        }
+        unsigned int fl[2] = {0, 0};
+        flags.download(fl, 2, s);
         FGB_CUDA(cudaStreamSynchronize(s));
-        if (ov) throw Error("internal", "NN-Descent pool overflow (" + std::to_string(ov) + " candidates)");
+        if (fl[0]) throw Error("internal", "NN-Descent pool overflow (" + std::to_string(fl[0]) + " candidates)");
+        if (!fl[1]) break;
+        // (the dev counters of the failed launch stay summed)
+        ck = false;
+        a.ck_test_fail = 0;
+        FGB_CUDA(cudaMemcpyAsync(d_changed, changed0.get(), sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
     }
     if (a.timing) {
         FGB_CUDA(cudaEventRecord(e1, s));

@@ -249,12 +249,6 @@ __host__ __device__ __forceinline__ size_t path_bytes(uint32_t vocab, uint32_t c
 
 // Stages sparse path `path` of query qi (build_query_vector: fp32 w * v,
 // a zero weight drops the path, corpus.cpp:86-103); returns sum of (w v)^2.
-// Odd multipliers of the cuckoo tables, tried in order until every query
-// term has a slot (a table at <= 1/4 load practically never needs the second).
-__device__ __constant__ const uint32_t kCuckooMul[8][2] = {
-    {0x9E3779B1u, 0x85EBCA77u}, {0xC2B2AE3Du, 0x27D4EB2Fu}, {0x165667B1u, 0xD3A2646Du}, {0xFD7046C5u, 0xB55A4F09u},
-    {0x2545F491u, 0x4F1BBCDDu}, {0x68E31DA5u, 0x1B873593u}, {0xCC9E2D51u, 0x7FEB352Du}, {0x846CA68Bu, 0xE6546B65u}};
-
 __device__ inline double stage_path(const DevQueries& q, const uint32_t* vocabs, const uint32_t* caps, uint64_t qi, int path,
                              unsigned char* mem, PathQ& P, uint32_t lane, bool cuckoo = false) {
     const uint64_t lb = path ? q.s_ptr[qi] : q.l_ptr[qi], le = path ? q.s_ptr[qi + 1] : q.l_ptr[qi + 1];
@@ -327,40 +321,7 @@ __device__ inline double stage_path(const DevQueries& q, const uint32_t* vocabs,
             tk[j - lb] = qidx[j];
             tv[j - lb] = v;
         }
-        bool ok = false;
-        for (int seed = 0; seed < 8 && !ok; ++seed) {
-            const uint32_t m1 = kCuckooMul[seed][0], m2 = kCuckooMul[seed][1], sh = P.hshift;
-            for (uint32_t j = lane; j < cap; j += 32) keys[j] = kEmpty;
-            __syncwarp();
-            uint32_t good = 1;
-            if (lane == 0) {
-                for (uint32_t j = 0; j < nt && good; ++j) {
-                    uint32_t key = tk[j];
-                    float val = tv[j];
-                    uint32_t pos = (key * m1) >> sh;
-                    good = 0;
-                    for (uint32_t kick = 0; kick < 4 * nt + 16; ++kick) {
-                        const uint32_t old = keys[pos];
-                        const float oldv = vals[pos];
-                        keys[pos] = key;
-                        vals[pos] = val;
-                        if (old == kEmpty) {
-                            good = 1;
-                            break;
-                        }
-                        key = old;
-                        val = oldv;
-                        const uint32_t p1 = (key * m1) >> sh;
-                        pos = pos == p1 ? (key * m2) >> sh : p1;
-                    }
-                }
-            }
-            ok = __shfl_sync(kFull, good, 0) != 0;
-            P.hm1 = m1;
-            P.hm2 = m2;
-            __syncwarp();
-        }
-        if (!ok) P.hm1 = 0;  // no table found: the caller fails the query
+        approx::cuckoo_fill(P, keys, vals, tk, tv, nt, cap, lane);
         return ss;
     }
     uint32_t* keys = reinterpret_cast<uint32_t*>(mem);

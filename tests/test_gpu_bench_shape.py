@@ -101,3 +101,19 @@ def test_knn_pass_forced_parts_identical(shape, ref, monkeypatch):
     g1 = fg.nn_descent_iterate(dev, *r0)
     _same_lists(g1, r1, "pass 1, 8 parts")
     assert g1[3] == r1[3]
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_knn_pass_lookup_variants_identical(shape, ref, monkeypatch, mode):
+    """The pass stages u's sparse rows as cuckoo tables (default); the
+    bitmap / filter + hash staging (FGB_KNN_CUCKOO=0) and the re-run after
+    failed tables (test hook FGB_KNN_CUCKOO=2: every node u % 7 == 3 fails,
+    the pass runs again without cuckoo tables and restores the replaced
+    count) give the same lists."""
+    c, dev, st = shape["c"], shape["dev"], shape["st"]
+    r0 = ref.knn_init(st, c.n, 64, 11, threads=THREADS)
+    r1 = ref.knn_iterate(st, *r0, threads=THREADS)
+    monkeypatch.setenv("FGB_KNN_CUCKOO", mode)
+    g1 = fg.nn_descent_iterate(dev, *r0)
+    _same_lists(g1, r1, f"pass 1, FGB_KNN_CUCKOO={mode}")
+    assert g1[3] == r1[3]
