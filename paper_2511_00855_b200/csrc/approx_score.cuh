@@ -257,6 +257,92 @@ __device__ __forceinline__ double sparse_group(const uint32_t* idx, const float*
     return mine;
 }
 
+// ---- sparse sketch bound (NN-Descent pass 1)
+// Every document carries a 512-byte SKETCH of its sparse paths: 2,048
+// buckets of 2 bits, bucket b holding q_b = ceil(max |v_t| / g_v) over the
+// terms t of the document in b (learned term t -> t & 2047, statistical term
+// t -> (t + 1024) & 2047; g_v = the corpus's max |value| / 3 with margin).
+// For a node u with bucket sums U_b = sum |u_t| quantised up to bytes
+// (uq_b g_u >= U_b),
+//     L(u, v) + S(u, v) <= sum_t |u_t| |v_t| <= sum_b U_b max_b |v|
+//                       <= g_u g_v sum_b uq_b q_b,
+// an exact integer dot (dp4a over the unpacked 2-bit lanes).  On pass 1's
+// random two-hop candidates it rejects ~3/4 of them without touching their
+// postings (C2 shape: the sparse part dominates the score), and one 16-byte
+// load per lane covers a candidate (16 candidates per round trip).
+constexpr uint32_t kSketchBuckets = 2048;
+constexpr uint32_t kSketchBytes = kSketchBuckets / 4;  // per document
+__device__ __forceinline__ uint32_t sketch_bucket(uint32_t t, int path) {
+    return (t + (path ? kSketchBuckets / 2 : 0u)) & (kSketchBuckets - 1);
+}
+// Packing: bucket 16 w + 4 t + i of a lane's 64 lives in byte i, bits 2t..2t+1
+// of the lane's word w; (word >> 2t) & 0x03030303 holds buckets 16 w + 4 t ..
+// + 3 as bytes, matching u's byte word 4 w + t.
+
+// Reduce-scatter of 16 per-lane u32 partial sums: row r's total ends in
+// lanes [2r, 2r + 2).
+__device__ __forceinline__ uint32_t reduce_scatter16_u32(uint32_t (&x)[16], uint32_t lane) {
+    const bool b4 = (lane >> 4) & 1u, b3 = (lane >> 3) & 1u, b2 = (lane >> 2) & 1u, b1 = (lane >> 1) & 1u;
+    uint32_t y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t send = b4 ? x[i] : x[i + 8];
+        y[i] = (b4 ? x[i + 8] : x[i]) + __shfl_xor_sync(kFull, send, 16);
+    }
+    uint32_t z[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t send = b3 ? y[i] : y[i + 4];
+        z[i] = (b3 ? y[i + 4] : y[i]) + __shfl_xor_sync(kFull, send, 8);
+    }
+    uint32_t w[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const uint32_t send = b2 ? z[i] : z[i + 2];
+        w[i] = (b2 ? z[i + 2] : z[i]) + __shfl_xor_sync(kFull, send, 4);
+    }
+    uint32_t r = (b1 ? w[1] : w[0]) + __shfl_xor_sync(kFull, b1 ? w[0] : w[1], 2);
+    r += __shfl_xor_sync(kFull, r, 1);
+    return r;
+}
+
+// Integer sketch dot sum_b uq_b q_b(node) for the F nodes held by lanes
+// 0..F-1; lane j receives node j's.  uq = u's quantised bucket sums in shared
+// memory (2,048 bytes); lane L covers buckets [64 L, 64 L + 64).
+__device__ __forceinline__ uint32_t sketch_group(const uint4* sketch, const uint32_t* uq, uint32_t node,
+                                                 uint32_t lane, uint32_t F) {
+    uint32_t mine = 0;
+#pragma unroll 1
+    for (uint32_t g = 0; g < F; g += 16) {
+        uint4 v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const uint32_t j = g + k;
+            const uint32_t nj = __shfl_sync(kFull, node, j & 31);
+            v[k] = __ldg(sketch + static_cast<uint64_t>(j < F ? nj : 0u) * (kSketchBytes / 16) + lane);
+        }
+        uint32_t part[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) part[k] = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const uint4 u4 = reinterpret_cast<const uint4*>(uq)[4 * lane + w];  // u's bytes 64 L + 16 w ..
+            const uint32_t uw[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint32_t word = w == 0 ? v[k].x : w == 1 ? v[k].y : w == 2 ? v[k].z : v[k].w;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) part[k] = __dp4a((word >> (2 * t)) & 0x03030303u, uw[t], part[k]);
+            }
+        }
+        const uint32_t r = reduce_scatter16_u32(part, lane);
+        const uint32_t k = lane - g;
+        const uint32_t got = __shfl_sync(kFull, r, (2 * k) & 31);
+        if (lane >= g && lane < g + 16) mine = got;
+    }
+    return mine;
+}
+
 template <int NQ4>
 __device__ __forceinline__ void dense_load(const DevCorpus& c, uint32_t node, uint32_t lane, float4 (&b)[NQ4]) {
     const float4* row = reinterpret_cast<const float4*>(c.dense + static_cast<uint64_t>(node) * c.dstride);

@@ -142,7 +142,67 @@ struct PassArgs {
     uint32_t ck_cap[2];          // cuckoo variant: table slots per path (power of two >= 4 max nnz)
     unsigned int* ck_fail;       // cuckoo variant: nodes without a table (the host re-runs the pass)
     uint32_t ck_test_fail;       // test hook (FGB_KNN_CUCKOO=2): nodes u % 7 == 3 fail their tables
+    // sparse sketch screening (approx_score.cuh sketch_group; nullptr: off)
+    const uint4* sketch;
+    const unsigned int* sk_gmax;  // bits of the corpus's max |sparse value| (the sketch scale)
+    uint32_t sk_off;              // shared-memory byte offset of u's quantised bucket sums
+    uint32_t sk_paths;            // bit 0: learned, bit 1: statistical
 };
+
+// The sketch scale g_v from the corpus's max |value| (identical in the
+// sketch build and in the bound).
+__device__ __forceinline__ double sketch_gv(unsigned int gmax_bits) {
+    return static_cast<double>(__uint_as_float(gmax_bits)) * 1.001 / 3.0;
+}
+
+// Corpus max |value| of one sparse path (non-negative floats order like their bits).
+__global__ void sketch_max_kernel(const float* v, uint64_t m, unsigned int* out) {
+    float mx = 0.f;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+        mx = fmaxf(mx, fabsf(v[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
+}
+
+// One warp per document: bucket maxima of |value| quantised up to 2 bits,
+// q = ceil(|v| / g_v) in 0..3 (so q g_v >= |v|), packed into the document's
+// 512-byte row.
+__global__ void sketch_build_kernel(DevCorpus c, uint32_t paths, const unsigned int* gmax, uint4* sk) {
+    extern __shared__ uint32_t skb[];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t doc = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp;
+    if (doc >= c.n) return;  // (warp-uniform; warps never synchronise with each other)
+    uint32_t* b = skb + warp * approx::kSketchBuckets;
+    for (uint32_t i = lane; i < approx::kSketchBuckets; i += 32) b[i] = 0;
+    __syncwarp();
+    const double gv = sketch_gv(*gmax);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        if (!((paths >> p) & 1u) || gv <= 0.0) continue;
+        const uint64_t off = p ? c.s_off[doc] : c.l_off[doc];
+        const uint32_t nnz = p ? c.s_nnz[doc] : c.l_nnz[doc];
+        const uint32_t* idx = p ? c.s_idx : c.l_idx;
+        const float* val = p ? c.s_val : c.l_val;
+        for (uint32_t j = lane; j < nnz; j += 32) {
+            const double x = static_cast<double>(fabsf(val[off + j])) / gv * (1.0 + 1e-12);
+            const uint32_t q = static_cast<uint32_t>(fmin(3.0, ceil(x)));
+            atomicMax(&b[approx::sketch_bucket(idx[off + j], p)], q);
+        }
+    }
+    __syncwarp();
+    uint32_t w[4];  // lane L: buckets 64 L + 16 w + 4 t + i -> word w, byte i, bits 2t
+#pragma unroll
+    for (int ww = 0; ww < 4; ++ww) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) word |= b[64 * lane + 16 * ww + 4 * t + i] << (8 * i + 2 * t);
+        w[ww] = word;
+    }
+    sk[doc * (approx::kSketchBytes / 16) + lane] = make_uint4(w[0], w[1], w[2], w[3]);
+}
 
 // Shared-memory bytes of one path's cuckoo table: keys, values, staged row.
 __host__ __device__ __forceinline__ size_t ck_bytes(uint32_t cap) {
@@ -151,7 +211,7 @@ __host__ __device__ __forceinline__ size_t ck_bytes(uint32_t cap) {
 
 enum : int {
     kKnPhInit = 0, kKnPhPool, kKnPhScore, kKnPhMerge, kKnPhExact, kKnPhFinal,  // cycles (thread 0)
-    kKnCand, kKnDense, kKnEnter, kKnRounds, kKnResolved, kKnCount   // counters
+    kKnCand, kKnDense, kKnEnter, kKnRounds, kKnResolved, kKnSketch, kKnCount   // counters
 };
 
 // Probes are bounded: a full table (a part far above its expected size)
@@ -460,6 +520,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     float* qd = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(S_mk + kSCap) + 15) & ~uintptr_t(15));
     approx::PathQ P[2];
     double eps = 0.0;
+    double sk_scale = 0.0;  // g_u g_v (sketch screening)
     if constexpr (NQ4 > 0) {
         for (uint32_t j = tid; j < a.c.dstride; j += nt) qd[j] = a.c.dense[u * a.c.dstride + j];
         for (int p = 0; p < 2; ++p) {
@@ -549,6 +610,45 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
             P[0].bm = bm;
             P[0].pre = pre;
             P[0].qv = qv;
+        }
+        if (a.sketch) {
+            // u's bucket sums U_b = sum |u_t| (fp32, pool table as scratch:
+            // it is initialised per part below), quantised up to bytes with
+            // g_u = max U_b * 1.001 / 255: uq_b g_u >= 1.0001 U_b (1 +- 1e-7)
+            // covers the fp32 sums' rounding (<= 240 terms: 1.5e-5)
+            __shared__ unsigned int sk_max;
+            float* ub = reinterpret_cast<float*>(keys);
+            for (uint32_t j = tid; j < approx::kSketchBuckets; j += nt) ub[j] = 0.f;
+            if (tid == 0) sk_max = 0;
+            __syncthreads();
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (!((a.sk_paths >> p) & 1u)) continue;
+                const uint64_t off = p ? a.c.s_off[u] : a.c.l_off[u];
+                const uint32_t nnz = p ? a.c.s_nnz[u] : a.c.l_nnz[u];
+                for (uint32_t j = tid; j < nnz; j += nt)
+                    atomicAdd(&ub[approx::sketch_bucket((p ? a.c.s_idx : a.c.l_idx)[off + j], p)],
+                              fabsf((p ? a.c.s_val : a.c.l_val)[off + j]));
+            }
+            __syncthreads();
+            float mx = 0.f;
+            for (uint32_t j = tid; j < approx::kSketchBuckets; j += nt) mx = fmaxf(mx, ub[j]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+            if ((tid & 31) == 0 && mx > 0.f) atomicMax(&sk_max, __float_as_uint(mx));
+            __syncthreads();
+            const float gu = __uint_as_float(sk_max) * 1.001f / 255.f;
+            uint32_t* uqw = reinterpret_cast<uint32_t*>(smem + a.sk_off);
+            for (uint32_t w = tid; w < approx::kSketchBuckets / 4; w += nt) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t q = gu > 0.f ? min(255u, static_cast<uint32_t>(ceilf(ub[4 * w + i] * 1.0001f / gu))) : 0u;
+                    word |= q << (8 * i);
+                }
+                uqw[w] = word;
+            }
+            sk_scale = static_cast<double>(gu) * sketch_gv(*a.sk_gmax) * (1.0 + 1e-12);
         }
         eps = a.eps32 * unorm * (1.0 + 1e-10) * a.max_dnorm +
               a.eps32 * sqrt(a.c.sqnorm[u]) * (1.0 + 1e-10) * a.max_norm +  // fp32 sparse products
@@ -671,12 +771,32 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
             // approximation is below it by more than both bounds never enters
             const double tau_lo = tau - (T_ex[k - 1] ? 0.0 : eps);
             const uint32_t fm = __ballot_sync(approx::kFull, cand);
-            if (fm) {  // warp-uniform
-                const uint32_t F = __popc(fm);
-                const uint32_t src = __fns(fm, 0, lane + 1);
-                const uint32_t cn = __shfl_sync(approx::kFull, id, src < 32 ? src : 0);
-                const bool mine = lane < F;
-                const uint4 mt = mine ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
+            uint32_t F = __popc(fm);
+            const uint32_t src = __fns(fm, 0, lane + 1);
+            uint32_t cn = __shfl_sync(approx::kFull, id, src < 32 ? src : 0);
+            bool mine = lane < F;
+            uint4 mt = mine ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
+            if (a.sketch && F) {  // warp-uniform
+                // sketch screening: candidates whose sparse bound + |u||v| is
+                // certified below the k-th never load their postings
+                const uint32_t sb = approx::sketch_group(a.sketch, reinterpret_cast<const uint32_t*>(smem + a.sk_off),
+                                                         cn, lane, F);
+                const bool pass = mine && !(score_upper_bound(unorm, (double)__uint_as_float(mt.w),
+                                                              static_cast<double>(sb) * sk_scale, 0.0) +
+                                                2.0 * eps < tau_lo);
+                const uint32_t pm = __ballot_sync(approx::kFull, pass);
+                if (lane == 0) count(kKnSketch, F - __popc(pm));
+                const uint32_t s2 = __fns(pm, 0, lane + 1);
+                const uint32_t sl = s2 < 32 ? s2 : 0;
+                cn = __shfl_sync(approx::kFull, cn, sl);
+                mt.x = __shfl_sync(approx::kFull, mt.x, sl);
+                mt.y = __shfl_sync(approx::kFull, mt.y, sl);
+                mt.z = __shfl_sync(approx::kFull, mt.z, sl);
+                mt.w = __shfl_sync(approx::kFull, mt.w, sl);
+                F = __popc(pm);
+                mine = lane < F;
+            }
+            if (F) {  // warp-uniform
                 if (a.prefetch && mine && lane >= approx::kSG) {
 #pragma unroll
                     for (int pth = 0; pth < 2; ++pth) {
@@ -898,7 +1018,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
 }
 
 size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uint32_t pool_cap,
-                 uint32_t l_vocab, const uint32_t* ck_cap) {
+                 uint32_t l_vocab, const uint32_t* ck_cap, bool sketch = false) {
     size_t b = (doc_stage_bytes(dstride, lcap, scap) + 15) & ~size_t(15);
     b += static_cast<size_t>(pool_cap) * 4 + 2 * (pool_cap / 32) * 4;
     b += (2 * k + kSCap) * 8 + (2 * k + kSCap) * 4;
@@ -909,6 +1029,7 @@ size_t pass_smem(uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t k, uin
         const size_t W = approx::bitmap_words(l_vocab);
         b += ((W + 3) & ~size_t(3)) * 4 + ((W + 7) & ~size_t(7)) * 2 + static_cast<size_t>(lcap) * 4;
     }
+    if (sketch) b = ((b + 15) & ~size_t(15)) + approx::kSketchBuckets;  // u's quantised bucket sums (last)
     return b;
 }
 
@@ -926,12 +1047,12 @@ uint32_t pool_slots(double items) {
 // overflows fails the pass loudly).
 constexpr size_t kSmemTwo = 113 * 1024;
 void pool_plan(uint64_t n, uint32_t k, uint32_t dstride, uint32_t lcap, uint32_t scap, uint32_t l_vocab,
-               const uint32_t* ck_cap, uint32_t& cap, uint32_t& nparts) {
+               const uint32_t* ck_cap, bool sketch, uint32_t& cap, uint32_t& nparts) {
     const double worst = static_cast<double>(std::min<uint64_t>(n, 4ull * k * k + k));
     for (nparts = 1;; nparts <<= 1) {
         const double per = nparts == 1 ? worst : worst / nparts + 4.0 * std::sqrt(worst / nparts) + 64.0;
         cap = pool_slots(per);
-        if (pass_smem(dstride, lcap, scap, k, cap, l_vocab, ck_cap) <= kSmemTwo || cap <= kPassThreads || nparts >= 64)
+        if (pass_smem(dstride, lcap, scap, k, cap, l_vocab, ck_cap, sketch) <= kSmemTwo || cap <= kPassThreads || nparts >= 64)
             return;
     }
 }
@@ -1056,6 +1177,34 @@ void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s) {
     FGB_LAUNCH("reverse_fill_kernel");
 }
 
+int knn_sketch_policy() {
+    const char* e = std::getenv("FGB_KNN_SKETCH");
+    return e ? std::atoi(e) : 1;
+}
+
+void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s) {
+    R.sk_paths = (c.max_lnnz ? 1u : 0u) | (c.max_snnz ? 2u : 0u);
+    if (!R.sk_paths || !c.dc.meta || pass_nq4(c.dstride) == 0) return;  // (exact-chain passes: no screening)
+    if (R.sketch.size() == c.n * (approx::kSketchBytes / 16)) return;
+    R.sketch.alloc(c.n * (approx::kSketchBytes / 16));
+    R.sk_gmax.alloc(1);
+    R.sk_gmax.zero(s);
+    if (c.max_lnnz)
+        sketch_max_kernel<<<1184, 256, 0, s>>>(c.dc.l_val, c.l_nnz_total4 * 4, R.sk_gmax.get());
+    if (c.max_snnz)
+        sketch_max_kernel<<<1184, 256, 0, s>>>(c.dc.s_val, c.s_nnz_total4 * 4, R.sk_gmax.get());
+    FGB_LAUNCH("sketch_max_kernel");
+    constexpr uint32_t kWarps = 4;  // 32 KB of bucket maxima per CTA
+    sketch_build_kernel<<<(unsigned)((c.n + kWarps - 1) / kWarps), 32 * kWarps, kWarps * approx::kSketchBuckets * 4, s>>>(
+        c.dc, R.sk_paths, R.sk_gmax.get(), R.sketch.get());
+    FGB_LAUNCH("sketch_build_kernel");
+}
+
+void knn_sketch_release(ReverseLists& R) {
+    R.sketch.release();
+    R.sk_gmax.release();
+}
+
 // The per-node two-hop join (knn_graph.cpp:91-142) for nodes [lo, hi) of the
 // snapshot g (with its reverse lists R) into rows [lo, hi) of next; adds the
 // number of replaced entries to *d_changed (device).
@@ -1127,11 +1276,12 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;
         a.ck_cap[0] = ck && !a.l_vocab && c.max_lnnz ? ck_cap(c.max_lnnz) : 0;
         a.ck_cap[1] = ck && c.max_snnz ? ck_cap(c.max_snnz) : 0;
-        pool_plan(g.n, k, c.dstride, lcap, scap, a.l_vocab, a.ck_cap, a.pool_cap, a.nparts);
-        if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap) > 227 * 1024) {
+        const bool sk = nq4 > 0 && R.sketch.size() == g.n * (approx::kSketchBytes / 16);
+        pool_plan(g.n, k, c.dstride, lcap, scap, a.l_vocab, a.ck_cap, sk, a.pool_cap, a.nparts);
+        if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap, sk) > 227 * 1024) {
             a.l_vocab = 0;
             a.ck_cap[0] = ck && c.max_lnnz ? ck_cap(c.max_lnnz) : 0;
-            pool_plan(g.n, k, c.dstride, lcap, scap, 0, a.ck_cap, a.pool_cap, a.nparts);
+            pool_plan(g.n, k, c.dstride, lcap, scap, 0, a.ck_cap, sk, a.pool_cap, a.nparts);
         }
         if (const char* e = std::getenv("FGB_KNN_PARTS")) {  // dev/test: force a part count (power of two)
             const uint32_t v = static_cast<uint32_t>(std::atoi(e));
@@ -1145,7 +1295,13 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         flags.zero(s);
         a.overflow = flags.get();
         a.ck_fail = flags.get() + 1;
-        sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap);
+        // (the sketch's u-side sums use the pool table as scratch: >= 2,048 slots)
+        const bool use_sk = sk && a.pool_cap >= approx::kSketchBuckets;
+        sm = pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap, use_sk);
+        a.sketch = use_sk ? R.sketch.get() : nullptr;
+        a.sk_gmax = use_sk ? R.sk_gmax.get() : nullptr;
+        a.sk_paths = R.sk_paths;
+        a.sk_off = use_sk ? static_cast<uint32_t>(sm - approx::kSketchBuckets) : 0;
         if (sm > 227 * 1024)
             throw Error("invalid-argument", "knn_k too large for the shared-memory pool (" +
                                                 std::to_string(sm) + " B)");
@@ -1181,10 +1337,10 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         std::fprintf(stderr,
                      "[knn pass] %llu nodes, %.1f ms, smem %zu B, pool_cap %u x %u parts | cycles/node: init %.0f pool %.0f "
                      "score %.0f merge %.0f exact %.0f final %.0f | per node: cand %.1f dense %.1f enter %.1f rounds %.1f "
-                     "resolved %.2f\n",
+                     "resolved %.2f sketch-rejected %.1f\n",
                      (unsigned long long)blocks, ms, sm, a.pool_cap, a.nparts, t[kKnPhInit] / nb, t[kKnPhPool] / nb,
                      t[kKnPhScore] / nb, t[kKnPhMerge] / nb, t[kKnPhExact] / nb, t[kKnPhFinal] / nb, t[kKnCand] / nb, t[kKnDense] / nb,
-                     t[kKnEnter] / nb, t[kKnRounds] / nb, t[kKnResolved] / nb);
+                     t[kKnEnter] / nb, t[kKnRounds] / nb, t[kKnResolved] / nb, t[kKnSketch] / nb);
     }
 }
 
@@ -1218,6 +1374,7 @@ uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s, Rever
 
 uint64_t knn_iterate_device(const fg_corpus& c, DevKnn& g, cudaStream_t s) {
     ReverseLists R;
+    if (knn_sketch_policy() >= 2) knn_sketch_prepare(c, R, s);
     DevKnn next;
     DevBuf<unsigned long long> changed;
     return knn_iterate_device(c, g, s, R, next, changed);
@@ -1270,10 +1427,18 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
     }
     DevKnn next;
     DevBuf<unsigned long long> d_changed;
+    const int sk_policy = knn_sketch_policy();
+    if (sk_policy >= 1) {
+        knn_sketch_prepare(c, R, s);
+        ht.mark("sketch");
+    }
     for (uint32_t it = 0; it < max_iterations; ++it) {
         const uint64_t changed = knn_iterate_device(c, g, s, R, next, d_changed);
         ht.mark("pass");
         ++passes;
+        // pass 1's candidates are random: the sketch bound rejects most of
+        // them; later passes score neighbourhoods, where it rarely does
+        if (it == 0 && sk_policy == 1) knn_sketch_release(R);
         if (static_cast<double>(changed) / denom < convergence) break;
         // After pass 1 the lists are neighbourhoods: later passes visit the
         // nodes in BFS order over them, so the CTAs resident at one time work

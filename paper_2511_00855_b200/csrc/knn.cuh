@@ -37,6 +37,11 @@ struct ReverseLists {
     // pass statistics (knn_build_device with a KnnStats): candidate / dense
     // row counters, device time of the pass kernels
     DevBuf<unsigned long long> counts;
+    // sparse sketches (512 B per document) and their scale for the pass
+    // kernel's sketch screening (knn_sketch_prepare; empty: off)
+    DevBuf<uint4> sketch;
+    DevBuf<unsigned int> sk_gmax;
+    uint32_t sk_paths = 0;
     double pass_ms = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     ReverseLists() = default;
@@ -59,6 +64,12 @@ struct KnnStats {
 // init_random_graph (knn_graph.cpp:52-73) into g (allocated n x k).
 void knn_init_device(const fg_corpus& c, uint32_t k, uint64_t seed, DevKnn& g, cudaStream_t s);
 void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s);
+// Sketch screening policy (FGB_KNN_SKETCH: 0 off, 1 = a build's first pass
+// (default), 2 = every pass incl. single fg_knn_iterate calls) and the
+// sketches themselves (built into R; released by knn_sketch_release).
+int knn_sketch_policy();
+void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s);
+void knn_sketch_release(ReverseLists& R);
 // The two-hop join for nodes [lo, hi) of g into the same rows of next.
 void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, uint64_t lo, uint64_t hi,
                     DevKnn& next, unsigned long long* d_changed, cudaStream_t s);

@@ -117,3 +117,22 @@ def test_knn_pass_lookup_variants_identical(shape, ref, monkeypatch, mode):
     g1 = fg.nn_descent_iterate(dev, *r0)
     _same_lists(g1, r1, f"pass 1, FGB_KNN_CUCKOO={mode}")
     assert g1[3] == r1[3]
+
+
+def test_knn_passes_sketch_screening_identical(shape, ref, monkeypatch):
+    """Sparse-sketch screening (knn.cu knn_sketch_prepare / approx_score.cuh
+    sketch_group: an integer upper bound of the sparse parts from 1,024-byte
+    bucket maxima) rejects candidates before their postings are read.  A build
+    screens its first pass; FGB_KNN_SKETCH=2 screens every pass, here three
+    passes from the reference's own snapshots, each identical to
+    nn_descent_iterate (knn_graph.cpp:75-148); FGB_KNN_SKETCH=0 too."""
+    c, dev, st = shape["c"], shape["dev"], shape["st"]
+    cur = ref.knn_init(st, c.n, 64, 13, threads=THREADS)
+    for it in range(3):
+        r1 = ref.knn_iterate(st, *cur, threads=THREADS)
+        for mode in ("2", "0"):
+            monkeypatch.setenv("FGB_KNN_SKETCH", mode)
+            g1 = fg.nn_descent_iterate(dev, *cur)
+            _same_lists(g1, r1, f"pass {it + 1}, FGB_KNN_SKETCH={mode}")
+            assert g1[3] == r1[3]
+        cur = r1[:3]

@@ -13,7 +13,7 @@ ap.add_argument("--docs", type=int, default=1000000)
 ap.add_argument("--repeat", type=int, default=1, help="build this many times in one process")
 ap.add_argument("--shape", default="C2", choices=["C2", "C3"], help="C3: + statistical vocab 831,592, nnz 40")
 a = ap.parse_args()
-p = A.synth_params(docs=a.docs, dense_dim=768, learned_vocab=30522, learned_nnz=120,
+p = A.synth_params(docs=a.docs, dense_dim=768, clusters=20, cluster_spread=0.25, learned_vocab=30522, learned_nnz=120,
                    statistical_vocab=831592 if a.shape == "C3" else 0, statistical_nnz=40, seed=1)
 c, kg, _ = synth.generate_corpus(p, 0)
 dc = fg.DeviceCorpus(c)
