@@ -13,6 +13,7 @@
 //      kept in shared memory (better: score desc, id asc); the result and the
 //      replaced count are written to the next buffer (knn_graph.cpp:122-141).
 #include <cub/cub.cuh>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cmath>
@@ -356,7 +357,7 @@ __device__ __forceinline__ uint32_t count_better(const double* sc, const uint32_
 // the list T (see the call site).  mrg: >= k + 1 words of scratch holding the
 // merged order's first k + 1 entries (bit 31: an S index, else a T index).
 template <int NQ4>
-__device__ void merge_certify_sorted(const PassArgs& a, const SmemQuery& sq, uint32_t m, uint32_t k, uint32_t n_c,
+__device__ void merge_certify_sorted(const PassArgs& a, const SmemQuery& sq, uint32_t m, uint32_t k, uint32_t n_res,
                                      double eps, uint32_t* keys, uint32_t* fbits, double* T_sc, const uint32_t* T_id,
                                      uint8_t* T_ex, uint8_t* T_mk, double* S_sc, uint32_t* S_id, uint8_t* S_ex,
                                      uint8_t* S_mk, uint32_t* mrg, uint32_t* n_mark) {
@@ -449,13 +450,129 @@ __device__ void merge_certify_sorted(const PassArgs& a, const SmemQuery& sq, uin
             }
         __syncthreads();
         if (!any_mark) break;
-        unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_c + 3) & ~3u));
-        const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_c + 3) & ~3u)) * 4;
+        unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_res + 3) & ~3u));
+        const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_res + 3) & ~3u)) * 4;
         resolve_marked<NQ4>(a, sq, S_mk, m, 0u, fbits, a.pool_cap / 16, n_mark, area, area_bytes, T_sc, T_ex, T_id,
                             S_sc, S_ex, S_id);
         resolve_marked<NQ4>(a, sq, T_mk, k, 0x80000000u, fbits, a.pool_cap / 16, n_mark, area, area_bytes, T_sc,
                             T_ex, T_id, S_sc, S_ex, S_id);
     }
+    __syncthreads();
+}
+
+constexpr uint32_t kSkFirst = 512;  // candidates moved to the front by sketch_order
+
+// Block-wide exclusive scan of two counters (blockDim.x <= 1024).
+__device__ __forceinline__ void block_excl_scan2(uint32_t& x, uint32_t& y, uint32_t* wsum) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t ix = x, iy = y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t tx = __shfl_up_sync(0xFFFFFFFFu, ix, o), ty = __shfl_up_sync(0xFFFFFFFFu, iy, o);
+        if (lane >= o) {
+            ix += tx;
+            iy += ty;
+        }
+    }
+    if (lane == 31) {
+        wsum[2 * warp] = ix;
+        wsum[2 * warp + 1] = iy;
+    }
+    __syncthreads();
+    uint32_t bx = 0, by = 0;
+    for (uint32_t w = 0; w < warp; ++w) {
+        bx += wsum[2 * w];
+        by += wsum[2 * w + 1];
+    }
+    __syncthreads();
+    x = bx + ix - x;
+    y = by + iy - y;
+}
+
+// Computes every candidate's sketch bound into bnd[0, n_c) and moves the
+// ~kSkFirst highest to the front of keys/bnd (in-place swap partition).
+// hist: 256 free words, hpos: kSCap free words.
+template <class Args>
+__device__ void sketch_order(const Args& a, uint32_t* keys, uint16_t* bnd, uint32_t n_c, double unorm, double eps,
+                             double sk_scale, const uint32_t* uq, uint32_t* hist, uint32_t* hpos, uint32_t lane) {
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    for (uint32_t b2 = 0; b2 < n_c; b2 += nt) {
+        const uint32_t s = b2 + tid;
+        const bool cand = s < n_c;  // (a prefix of each warp)
+        const uint32_t cn = cand ? keys[s] : 0u;
+        const uint32_t F = __popc(__ballot_sync(approx::kFull, cand));
+        if (!F) continue;  // warp-uniform
+        const uint4 mt = cand ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
+        const uint32_t sb = approx::sketch_group(a.sketch, uq, cn, lane, F);
+        if (cand) {
+            const double b = score_upper_bound(unorm, (double)__uint_as_float(mt.w), static_cast<double>(sb) * sk_scale,
+                                               0.0) + 2.0 * eps;
+            bnd[s] = __bfloat16_as_ushort(__float2bfloat16_ru(__double2float_ru(b)));
+        }
+    }
+    if (n_c <= kSkFirst) {
+        __syncthreads();
+        return;
+    }
+    // radix select of the kSkFirst-th largest key (bf16 bits of non-negative
+    // values order as integers): high byte, then low byte within its bin
+    __shared__ uint32_t sel_hi, sel_above, sel_t, sel_m1, sel_ws[64];
+    for (uint32_t i = tid; i < 256; i += nt) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t s = tid; s < n_c; s += nt) atomicAdd(&hist[bnd[s] >> 8], 1u);
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t acc = 0, b = 255;
+        while (b > 0 && acc + hist[b] < kSkFirst) acc += hist[b--];
+        sel_hi = b;
+        sel_above = acc;
+    }
+    __syncthreads();
+    const uint32_t hi = sel_hi;
+    for (uint32_t i = tid; i < 256; i += nt) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t s = tid; s < n_c; s += nt)
+        if ((bnd[s] >> 8) == hi) atomicAdd(&hist[bnd[s] & 0xFFu], 1u);
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t acc = sel_above, b = 255;
+        while (b > 0 && acc + hist[b] < kSkFirst) acc += hist[b--];
+        sel_t = (hi << 8) | b;
+        sel_m1 = 0;
+    }
+    __syncthreads();
+    const uint32_t T = sel_t;
+    uint32_t m1c = 0;
+    for (uint32_t s = tid; s < n_c; s += nt) m1c += bnd[s] >= T;
+    m1c = __reduce_add_sync(0xFFFFFFFFu, m1c);
+    if (lane == 0 && m1c) atomicAdd(&sel_m1, m1c);
+    __syncthreads();
+    const uint32_t m1 = sel_m1;
+    if (m1 > kSCap) return;  // (ties at the threshold: stays unordered; CTA-uniform)
+    // swap the r-th misplaced low (position < m1, key < T) with the r-th
+    // misplaced high (position >= m1, key >= T); contiguous chunks per thread
+    const uint32_t chunk = (n_c + nt - 1) / nt;
+    const uint32_t c0 = min(n_c, tid * chunk), c1 = min(n_c, c0 + chunk);
+    uint32_t nh = 0, nl = 0;
+    for (uint32_t s = c0; s < c1; ++s) {
+        const bool h = bnd[s] >= T;
+        nh += h && s >= m1;
+        nl += !h && s < m1;
+    }
+    block_excl_scan2(nh, nl, sel_ws);
+    for (uint32_t s = c0; s < c1; ++s)
+        if (s >= m1 && bnd[s] >= T) hpos[nh++] = s;
+    __syncthreads();
+    for (uint32_t s = c0; s < c1; ++s)
+        if (s < m1 && bnd[s] < T) {
+            const uint32_t hp = hpos[nl++];
+            const uint32_t tk = keys[s];
+            keys[s] = keys[hp];
+            keys[hp] = tk;
+            const uint16_t tb = bnd[s];
+            bnd[s] = bnd[hp];
+            bnd[hp] = tb;
+        }
     __syncthreads();
 }
 
@@ -756,6 +873,24 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     __syncthreads();
     const uint32_t n_c = n_cand;
     cand_total += n_c;
+    // Sketch ORDER (NQ4 > 0 with sketches, when the pool has room): every
+    // candidate's sketch bound is computed first and stored (bf16 rounded
+    // up, above the compacted list); the ~kSkFirst candidates with the
+    // highest bounds are swapped to the front, so the first round's exact
+    // scores lift the k-th entry close to its final value and the others
+    // are screened against it by their stored bounds.  (The result is the
+    // top-k of the set either way; only the work changes.)
+    uint16_t* bnd = nullptr;
+    uint32_t n_res = n_c;  // words of keys[] in use (resolutions stage rows above them)
+    if constexpr (NQ4 > 0) {
+        const uint32_t nc_al = (n_c + 1) & ~1u;
+        if (a.sketch && n_c > 0 && ((nc_al + nc_al / 2 + 3) & ~3u) <= a.pool_cap) {
+            bnd = reinterpret_cast<uint16_t*>(keys + nc_al);
+            n_res = nc_al + nc_al / 2;
+            sketch_order(a, keys, bnd, n_c, unorm, eps, sk_scale, reinterpret_cast<const uint32_t*>(smem + a.sk_off),
+                         reinterpret_cast<uint32_t*>(S_sc), S_id, lane);
+        }
+    }
     uint32_t round = 0;
     for (uint32_t base = 0; base < n_c; ++round) {
       const uint32_t grow = part > 0 ? uint32_t(kSRounds) : round == 0 ? 1u : round == 1 ? 2u : uint32_t(kSRounds);
@@ -770,13 +905,20 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
             // the k-th entry's value is exact or within eps: a candidate whose
             // approximation is below it by more than both bounds never enters
             const double tau_lo = tau - (T_ex[k - 1] ? 0.0 : eps);
-            const uint32_t fm = __ballot_sync(approx::kFull, cand);
+            // stored sketch bounds (+ |u||v| + 2 eps, rounded up) screen first
+            const bool live = cand && !(bnd && static_cast<double>(__bfloat162float(
+                                                   __ushort_as_bfloat16(bnd[s]))) < tau_lo);
+            if (a.timing && bnd) {
+                const uint32_t rej = __popc(__ballot_sync(approx::kFull, cand && !live));
+                if (lane == 0) count(kKnSketch, rej);
+            }
+            const uint32_t fm = __ballot_sync(approx::kFull, live);
             uint32_t F = __popc(fm);
             const uint32_t src = __fns(fm, 0, lane + 1);
             uint32_t cn = __shfl_sync(approx::kFull, id, src < 32 ? src : 0);
             bool mine = lane < F;
             uint4 mt = mine ? __ldg(a.c.meta + cn) : make_uint4(0, 0, 0, 0);
-            if (a.sketch && F) {  // warp-uniform
+            if (a.sketch && !bnd && F) {  // warp-uniform
                 // sketch screening: candidates whose sparse bound + |u||v| is
                 // certified below the k-th never load their postings
                 const uint32_t sb = approx::sketch_group(a.sketch, reinterpret_cast<const uint32_t*>(smem + a.sk_off),
@@ -877,7 +1019,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
                 // of the list are never resolved.  Loops until nothing is
                 // uncertain (every round resolves at least one approximation).
                 sorted = true;
-                merge_certify_sorted<NQ4>(a, sq, m, k, n_c, eps, keys, fbits, T_sc, T_id, T_ex, T_mk, S_sc, S_id,
+                merge_certify_sorted<NQ4>(a, sq, m, k, n_res, eps, keys, fbits, T_sc, T_id, T_ex, T_mk, S_sc, S_id,
                                           S_ex, S_mk, reinterpret_cast<uint32_t*>(T2_sc), &n_mark);
             }
         }
@@ -914,8 +1056,8 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
                 if (tid == 0) count(kKnResolved, n_mark + t_marked);
                 // resolve through rows staged above the compacted candidate
                 // list (the pool's upper part and its flag words are free)
-                unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_c + 3) & ~3u));
-                const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_c + 3) & ~3u)) * 4;
+                unsigned char* area = reinterpret_cast<unsigned char*>(keys + ((n_res + 3) & ~3u));
+                const size_t area_bytes = static_cast<size_t>(a.pool_cap - ((n_res + 3) & ~3u)) * 4;
                 resolve_marked<NQ4>(a, sq, S_mk, m, 0u, fbits, a.pool_cap / 16, &n_mark, area, area_bytes, T_sc,
                                     T_ex, T_id, S_sc, S_ex, S_id);
                 resolve_marked<NQ4>(a, sq, T_mk, k, 0x80000000u, fbits, a.pool_cap / 16, &n_mark, area, area_bytes,
