@@ -244,8 +244,11 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
                               const uint32_t* T_id, double* S_sc, uint8_t* S_ex, const uint32_t* S_id) {
     const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const uint32_t rs = a.c.dstride + 1, n4 = a.c.dstride >> 2;
-    const uint32_t cap = static_cast<uint32_t>(area_bytes / (rs * 4ull));
+    // rows + each entry's two sparse-chain results (the dense and the sparse
+    // chains of an entry run on different threads)
+    const uint32_t cap = area_bytes < 16 ? 0u : static_cast<uint32_t>((area_bytes - 16) / (rs * 4ull + 16));
     float* rows = reinterpret_cast<float*>(area);
+    double* xsp = reinterpret_cast<double*>(area + ((static_cast<size_t>(cap) * rs * 4 + 15) & ~size_t(15)));
     auto node_of = [&](uint32_t code) { return (code >> 31) ? T_id[code & 0x7FFFFFFFu] : S_id[code]; };
     if (cap == 0) {  // no room for a row (tiny pools): the chain from global memory
         for (uint32_t r = tid; r < n; r += nt) {
@@ -283,29 +286,47 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
             }
         }
         __syncthreads();
-        for (uint32_t r = tid; r < nb; r += nt) {
-            const uint32_t code = fix[b0 + r];
-            const uint32_t node = node_of(code);
-            const float* row = rows + r * rs;
-            double acc = 0.0;
-#pragma unroll 8
-            for (uint32_t j = 0; j < a.c.dstride; ++j)
-                acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(row[j])));
-            acc = __dadd_rn(acc, sq.lmask ? sparse_chain(a.c.l_idx, a.c.l_val, a.c.l_off[node], a.c.l_nnz[node],
-                                                         sq.lkeys, sq.lvals, sq.lmask, sq.lfilt)
-                                          : 0.0);
-            acc = __dadd_rn(acc, sq.smask ? sparse_chain(a.c.s_idx, a.c.s_val, a.c.s_off[node], a.c.s_nnz[node],
-                                                         sq.skeys, sq.svals, sq.smask, sq.sfilt)
-                                          : 0.0);
-            if (code >> 31) {
-                T_sc[code & 0x7FFFFFFFu] = acc;
-                T_ex[code & 0x7FFFFFFFu] = 1;
-            } else {
-                S_sc[code] = acc;
-                S_ex[code] = 1;
+        // the three chains of an entry are independent (hybrid_score only
+        // adds their results in order): per sub-batch of up to nt/3 entries,
+        // thread r runs entry r's dense chain while threads nbs + r and
+        // 2 nbs + r run its learned and statistical chains
+        const uint32_t sub = nt / 3;
+        for (uint32_t s0 = 0; s0 < nb; s0 += sub) {
+            const uint32_t nbs = min(sub, nb - s0);
+            if (tid >= nbs && tid < 3 * nbs) {
+                const bool lp = tid < 2 * nbs;
+                const uint32_t r = s0 + (lp ? tid - nbs : tid - 2 * nbs);
+                const uint32_t node = node_of(fix[b0 + r]);
+                double x = 0.0;
+                if (lp ? sq.lmask != 0 : sq.smask != 0)
+                    x = sparse_chain(lp ? a.c.l_idx : a.c.s_idx, lp ? a.c.l_val : a.c.s_val,
+                                     lp ? a.c.l_off[node] : a.c.s_off[node], lp ? a.c.l_nnz[node] : a.c.s_nnz[node],
+                                     lp ? sq.lkeys : sq.skeys, lp ? sq.lvals : sq.svals, lp ? sq.lmask : sq.smask,
+                                     lp ? sq.lfilt : sq.sfilt);
+                xsp[2 * (r - s0) + (lp ? 0 : 1)] = x;
             }
+            double acc = 0.0;
+            if (tid < nbs) {
+                const float* row = rows + (s0 + tid) * rs;
+#pragma unroll 8
+                for (uint32_t j = 0; j < a.c.dstride; ++j)
+                    acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(row[j])));
+            }
+            __syncthreads();
+            if (tid < nbs) {
+                const uint32_t code = fix[b0 + s0 + tid];
+                acc = __dadd_rn(acc, xsp[2 * tid]);
+                acc = __dadd_rn(acc, xsp[2 * tid + 1]);
+                if (code >> 31) {
+                    T_sc[code & 0x7FFFFFFFu] = acc;
+                    T_ex[code & 0x7FFFFFFFu] = 1;
+                } else {
+                    S_sc[code] = acc;
+                    S_ex[code] = 1;
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
