@@ -417,9 +417,14 @@ void corpus_append(fg_corpus& c, const fg_corpus_view& v) {
     {
         DevBuf<float> dense(n * c.dstride);
         FGB_CUDA(cudaMemcpyAsync(dense.get(), c.dense.get(), n0 * c.dstride * 4, cudaMemcpyDeviceToDevice, s));
-        std::vector<float> pad(b * c.dstride, 0.0f);
-        for (uint64_t i = 0; i < b; ++i) std::memcpy(pad.data() + i * c.dstride, v.dense + i * c.dim, c.dim * 4);
-        FGB_CUDA(cudaMemcpyAsync(dense.get() + n0 * c.dstride, pad.data(), pad.size() * 4, cudaMemcpyHostToDevice, s));
+        if (c.dim == c.dstride) {  // (rows need no padding: straight from the caller's array)
+            FGB_CUDA(cudaMemcpyAsync(dense.get() + n0 * c.dstride, v.dense, b * c.dim * 4, cudaMemcpyHostToDevice, s));
+        } else {
+            std::vector<float> pad(b * c.dstride, 0.0f);
+            for (uint64_t i = 0; i < b; ++i) std::memcpy(pad.data() + i * c.dstride, v.dense + i * c.dim, c.dim * 4);
+            FGB_CUDA(cudaMemcpyAsync(dense.get() + n0 * c.dstride, pad.data(), pad.size() * 4, cudaMemcpyHostToDevice, s));
+            FGB_CUDA(cudaStreamSynchronize(s));  // (pad dies here)
+        }
         FGB_CUDA(cudaStreamSynchronize(s));
         c.dense = std::move(dense);
     }

@@ -266,6 +266,15 @@ void check_sparse(const fg_sparse_view& sv, uint64_t i, const std::string& where
     }
 }
 
+// check_sparse's conditions without building messages (the common, valid case)
+bool sparse_ok(const fg_sparse_view& sv, uint64_t i) {
+    if (!sv.ptr) return true;
+    for (uint64_t j = sv.ptr[i]; j < sv.ptr[i + 1]; ++j)
+        if ((j > sv.ptr[i] && sv.idx[j] <= sv.idx[j - 1]) || !std::isfinite(sv.val[j]) || sv.val[j] == 0.0f)
+            return false;
+    return true;
+}
+
 void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert_params& p) {
     fg_corpus& c = *ix.corpus;
     cudaStream_t s = c.stream;
@@ -280,18 +289,27 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
     // ---- validate before touching anything (update.cpp:43-63)
     std::unordered_set<uint64_t> ids(c.doc_id.begin(), c.doc_id.end());
     std::vector<uint64_t> doc_id(batch);
+    // value checks of every row on host threads; the errors are raised below
+    // in the reference's order (first offending doc, its first failed check)
+    std::vector<uint8_t> bad(batch, 0);
+    parallel_rows(batch, [&](uint64_t i) {
+        bool ok = true;
+        for (uint32_t j = 0; j < in.dense_dim && ok; ++j) ok = std::isfinite(in.dense[i * in.dense_dim + j]);
+        bad[i] = !(ok && sparse_ok(in.learned, i) && sparse_ok(in.statistical, i));
+    });
     for (uint64_t i = 0; i < batch; ++i) {
         doc_id[i] = in.doc_id ? in.doc_id[i] : n_old + i;
-        const std::string where = "doc " + std::to_string(doc_id[i]);
-        if (ids.count(doc_id[i])) throw Error("duplicate-id", where + ": id already in the index");
+        auto where = [&] { return "doc " + std::to_string(doc_id[i]); };  // (built only for an error)
+        if (ids.count(doc_id[i])) throw Error("duplicate-id", where() + ": id already in the index");
         if (in.dense_dim != c.dim)
-            throw Error("dim-mismatch", where + ": dense dimension " + std::to_string(in.dense_dim) +
+            throw Error("dim-mismatch", where() + ": dense dimension " + std::to_string(in.dense_dim) +
                                             " differs from corpus " + std::to_string(c.dim));
+        if (!bad[i]) continue;
         for (uint32_t j = 0; j < in.dense_dim; ++j)
             if (!std::isfinite(in.dense[i * in.dense_dim + j]))
-                throw Error("nonfinite-value", where + ": dense holds a non-finite value");
-        check_sparse(in.learned, i, where, "learned");
-        check_sparse(in.statistical, i, where, "statistical");
+                throw Error("nonfinite-value", where() + ": dense holds a non-finite value");
+        check_sparse(in.learned, i, where(), "learned");
+        check_sparse(in.statistical, i, where(), "statistical");
     }
     {  // update.cpp:58-62 reports the first doc whose id occurs earlier in the batch
         std::unordered_set<uint64_t> seen;
@@ -318,12 +336,12 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
         return out;
     };
     const HostList kws = sorted_unique(in.keywords, true), ents = sorted_unique(in.entities, false);
+
     fg_corpus_view v = in;
     v.doc_id = doc_id.data();
     v.deleted = nullptr;
     v.keywords = fg_list_view{kws.ptr.data(), kws.idx.data()};
     v.entities = fg_list_view{ents.ptr.data(), ents.idx.data()};
-
     mark("validate");
     // ---- append the documents first (update.cpp:94-103): the new rows have no
     // edges yet, so (a) cannot reach them, and (b) reads them in place
@@ -493,7 +511,8 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
     const uint64_t n = n_old + batch;
     ix.semantic_h.resize(n * d);
     std::vector<std::vector<uint32_t>> new_kw(batch);
-    for (uint64_t i = 0; i < batch; ++i) {
+    std::vector<uint8_t> short_list(batch, 0);
+    parallel_rows(batch, [&](uint64_t i) {  // (rows independent: node i writes only its own lists)
         std::vector<uint32_t> list;
         list.reserve(d);
         auto has = [&](uint32_t id) { return std::find(list.begin(), list.end(), id) != list.end(); };
@@ -510,11 +529,16 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
             if (list.size() >= d) break;
             if (!has(id)) list.push_back(id);
         }
-        if (list.size() != d) throw Error("invariant-violation", "insert produced a short semantic list");
+        if (list.size() != d) {
+            short_list[i] = 1;
+            return;
+        }
         std::copy(list.begin(), list.end(), ix.semantic_h.begin() + (n_old + i) * d);
         for (uint32_t id : recycled[i])
             if (!has(id)) new_kw[i].push_back(id);
-    }
+    });
+    for (uint8_t sh : short_list)
+        if (sh) throw Error("invariant-violation", "insert produced a short semantic list");
 
     mark("new lists");
     // ---- existing nodes: weakest reverse slot replacement (update.cpp:167-193),
@@ -546,15 +570,41 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
         fg_pair_scores(&c, pa.data(), pb.data(), pa.size(), ps.data()) != FG_OK)
         throw Error(fg_last_error_code(), fg_last_error_message());
     // current score of each reverse slot of w (slot_base[w] + sl - half),
-    // updated in place as slots are replaced (update.cpp:167-193)
-    for (uint64_t i = 0; i < batch; ++i) {
-        const uint32_t u = static_cast<uint32_t>(n_old + i);
+    // updated in place as slots are replaced (update.cpp:167-193).  An edge
+    // (u -> w) reads and writes only w's list and slot scores, so the edges
+    // are grouped by w — each group keeping the reference's (u, q) order —
+    // and the groups run on host threads.
+    std::vector<uint32_t> touched;  // existing nodes with kept edges, first-touch order
+    std::vector<uint32_t> gcount;
+    std::vector<uint32_t> gidx(n_old, ~0u);
+    for (uint64_t i = 0; i < batch; ++i)
+        for (uint32_t w : kept[i])
+            if (w < n_old) {
+                if (gidx[w] == ~0u) {
+                    gidx[w] = static_cast<uint32_t>(touched.size());
+                    touched.push_back(w);
+                    gcount.push_back(0);
+                }
+                ++gcount[gidx[w]];
+            }
+    std::vector<uint64_t> gstart(touched.size() + 1, 0);
+    for (size_t g = 0; g < touched.size(); ++g) gstart[g + 1] = gstart[g] + gcount[g];
+    std::vector<std::pair<uint32_t, uint32_t>> gedge(gstart.back());  // (i, q) per group, in order
+    for (uint64_t i = 0; i < batch; ++i)
         for (size_t q = 0; q < kept[i].size(); ++q) {
             const uint32_t w = kept[i][q];
-            if (w >= n_old) continue;
-            uint32_t* sem = ix.semantic_h.data() + static_cast<uint64_t>(w) * d;
+            if (w < n_old) gedge[gstart[gidx[w]]++] = {static_cast<uint32_t>(i), static_cast<uint32_t>(q)};
+        }
+    for (size_t g = touched.size(); g > 0; --g) gstart[g] = gstart[g - 1];  // (restore the starts)
+    gstart[0] = 0;
+    parallel_rows(touched.size(), [&](uint64_t g) {
+        const uint32_t w = touched[g];
+        uint32_t* sem = ix.semantic_h.data() + static_cast<uint64_t>(w) * d;
+        double* sc = ps.data() + slot_base[w];
+        for (uint64_t e = gstart[g]; e < gstart[g + 1]; ++e) {
+            const auto [i, q] = gedge[e];
+            const uint32_t u = static_cast<uint32_t>(n_old + i);
             if (std::find(sem, sem + d, u) != sem + d) continue;
-            double* sc = ps.data() + slot_base[w];
             const size_t weakest = static_cast<size_t>(std::min_element(sc, sc + (d - half)) - sc);
             const double incoming = ps[edge_pair[i][q]];
             if (incoming > sc[weakest]) {
@@ -562,7 +612,7 @@ void insert_batch_device(fg_index& ix, const fg_corpus_view& in, const fg_insert
                 sc[weakest] = incoming;
             }
         }
-    }
+    });
 
     mark("reverse slots");
     // ---- keyword and logical edges, entity map, norm order; device refresh

@@ -1348,6 +1348,7 @@ int knn_sketch_policy() {
 void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s) {
     R.sk_paths = (c.max_lnnz ? 1u : 0u) | (c.max_snnz ? 2u : 0u);
     if (!R.sk_paths || !c.dc.meta || pass_nq4(c.dstride) == 0) return;  // (exact-chain passes: no screening)
+    R.sk_on = true;
     if (R.sketch.size() == c.n * (approx::kSketchBytes / 16)) return;
     R.sketch.alloc(c.n * (approx::kSketchBytes / 16));
     R.sk_gmax.alloc(1);
@@ -1363,10 +1364,7 @@ void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s) {
     FGB_LAUNCH("sketch_build_kernel");
 }
 
-void knn_sketch_release(ReverseLists& R) {
-    R.sketch.release();
-    R.sk_gmax.release();
-}
+void knn_sketch_disable(ReverseLists& R) { R.sk_on = false; }
 
 // The per-node two-hop join (knn_graph.cpp:91-142) for nodes [lo, hi) of the
 // snapshot g (with its reverse lists R) into rows [lo, hi) of next; adds the
@@ -1419,10 +1417,12 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
     bool ck = nq4 > 0;
     if (const char* e = std::getenv("FGB_KNN_CUCKOO"); e && e[0] == '0') ck = false;
     if (const char* e = std::getenv("FGB_KNN_CUCKOO"); e && e[0] == '2') a.ck_test_fail = 1;
-    DevBuf<unsigned int> flags(2);  // [0] pool overflow, [1] nodes without a cuckoo table
-    DevBuf<unsigned long long> changed0;
+    // (kept in R across passes: a device free synchronises the whole device)
+    DevBuf<unsigned int>& flags = R.flags;  // [0] pool overflow, [1] nodes without a cuckoo table
+    flags.ensure(2);
+    DevBuf<unsigned long long>& changed0 = R.changed0;
     if (ck) {
-        changed0.alloc(1);
+        changed0.ensure(1);
         FGB_CUDA(cudaMemcpyAsync(changed0.get(), d_changed, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
     }
     const uint64_t blocks = hi - lo;
@@ -1439,7 +1439,7 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
         a.l_vocab = c.l_vocab <= 65536 ? c.l_vocab : 0;
         a.ck_cap[0] = ck && !a.l_vocab && c.max_lnnz ? ck_cap(c.max_lnnz) : 0;
         a.ck_cap[1] = ck && c.max_snnz ? ck_cap(c.max_snnz) : 0;
-        const bool sk = nq4 > 0 && R.sketch.size() == g.n * (approx::kSketchBytes / 16);
+        const bool sk = nq4 > 0 && R.sk_on && R.sketch.size() == g.n * (approx::kSketchBytes / 16);
         pool_plan(g.n, k, c.dstride, lcap, scap, a.l_vocab, a.ck_cap, sk, a.pool_cap, a.nparts);
         if (pass_smem(c.dstride, lcap, scap, k, a.pool_cap, a.l_vocab, a.ck_cap, sk) > 227 * 1024) {
             a.l_vocab = 0;
@@ -1601,7 +1601,7 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
         ++passes;
         // pass 1's candidates are random: the sketch bound rejects most of
         // them; later passes score neighbourhoods, where it rarely does
-        if (it == 0 && sk_policy == 1) knn_sketch_release(R);
+        if (it == 0 && sk_policy == 1) knn_sketch_disable(R);
         if (static_cast<double>(changed) / denom < convergence) break;
         // After pass 1 the lists are neighbourhoods: later passes visit the
         // nodes in BFS order over them, so the CTAs resident at one time work

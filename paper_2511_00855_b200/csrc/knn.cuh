@@ -42,6 +42,11 @@ struct ReverseLists {
     DevBuf<uint4> sketch;
     DevBuf<unsigned int> sk_gmax;
     uint32_t sk_paths = 0;
+    bool sk_on = false;  // screening enabled for the next passes
+    // pass flags (overflow, failed cuckoo tables) and the replaced count
+    // before a pass (its re-run restores it)
+    mutable DevBuf<unsigned int> flags;
+    mutable DevBuf<unsigned long long> changed0;
     double pass_ms = 0.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     ReverseLists() = default;
@@ -66,10 +71,13 @@ void knn_init_device(const fg_corpus& c, uint32_t k, uint64_t seed, DevKnn& g, c
 void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s);
 // Sketch screening policy (FGB_KNN_SKETCH: 0 off, 1 = a build's first pass
 // (default), 2 = every pass incl. single fg_knn_iterate calls) and the
-// sketches themselves (built into R; released by knn_sketch_release).
+// sketches themselves (built into R).
 int knn_sketch_policy();
 void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s);
-void knn_sketch_release(ReverseLists& R);
+// Stops the screening for the next passes; the sketches stay allocated until R
+// dies (a device free synchronises the whole device, which would stall the
+// insert path's concurrent search behind this pass).
+void knn_sketch_disable(ReverseLists& R);
 // The two-hop join for nodes [lo, hi) of g into the same rows of next.
 void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, uint64_t lo, uint64_t hi,
                     DevKnn& next, unsigned long long* d_changed, cudaStream_t s);
