@@ -1340,6 +1340,8 @@ void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s) {
     FGB_LAUNCH("reverse_fill_kernel");
 }
 
+constexpr uint64_t kSketchMinNodes = 8192;
+
 int knn_sketch_policy() {
     const char* e = std::getenv("FGB_KNN_SKETCH");
     return e ? std::atoi(e) : 1;
@@ -1348,6 +1350,10 @@ int knn_sketch_policy() {
 void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s) {
     R.sk_paths = (c.max_lnnz ? 1u : 0u) | (c.max_snnz ? 2u : 0u);
     if (!R.sk_paths || !c.dc.meta || pass_nq4(c.dstride) == 0) return;  // (exact-chain passes: no screening)
+    // small corpora: a pass is a few launch latencies, the sketches' build
+    // and allocation would add to it (the reference's 2,400-doc insert
+    // criterion runs in ~5 ms)
+    if (c.n < kSketchMinNodes) return;
     R.sk_on = true;
     if (R.sketch.size() == c.n * (approx::kSketchBytes / 16)) return;
     R.sketch.alloc(c.n * (approx::kSketchBytes / 16));
