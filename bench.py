@@ -218,17 +218,21 @@ def build_rooflines(fg, ix, corpus, stages):
     if bs["pass_seconds"] > 0:
         nl = corpus.learned.ptr[-1] / corpus.n
         ns = corpus.statistical.ptr[-1] / corpus.n
-        gathered = bs["candidates"] * 8 * (nl + ns) + bs["dense_rows"] * 4 * corpus.dense_dim
+        # postings of every candidate the pass-1 sketches did not reject, the
+        # 512-byte sketch of every sketched candidate, the dense rows read
+        gathered = ((bs["candidates"] - bs["sketch_rejected"]) * 8 * (nl + ns) + bs["sketched"] * 512
+                    + bs["dense_rows"] * 4 * corpus.dense_dim)
         alg = bs["candidates"] * R
         out["knn"] = {
             "bound": "hbm", "kernel": "knn_pass_kernel", "passes": bs["passes"], "pair_scores": bs["candidates"],
             "dense_rows_read": bs["dense_rows"], "device_seconds": round(bs["pass_seconds"], 3),
+            "sketched": bs["sketched"], "sketch_rejected": bs["sketch_rejected"],
             "alg_bytes": int(alg), "achieved": round(alg / bs["pass_seconds"] / 1e9, 1), "peak": peak,
             "peak_kind": kind, "unit": "GB/s", "frac": round(alg / bs["pass_seconds"] / 1e9 / peak, 4),
             "gathered_bytes": int(gathered),
             "gathered_frac": round(gathered / bs["pass_seconds"] / 1e9 / peak, 4),
-            "traffic_note": "pass 1 at 200K docs under ncu: 2.75 TB DRAM in 1.05 s = 0.40 of peak "
-                            "(profiles/r02_knn_pass1_ncu.md)",
+            "traffic_note": "pass 1 at 200K docs under ncu (sketch screening): 1.55 TB DRAM in 0.72 s = 0.33 "
+                            "of peak (profiles/r02_knn_sketch_ncu.md)",
             "note": "alg_bytes counts every scored pair at full row bytes; the certified screening reads the "
                     "dense row of only dense_rows_read of them"}
     tc = fg.refine_tc_stats(reset=True)

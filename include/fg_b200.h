@@ -316,6 +316,10 @@ int fg_index_build_times(const fg_index* ix, double* seconds5);
  * after the certified screening, device microseconds of the pass kernels};
  * zeros for other builds.  Feeds the build roofline of bench.py. */
 int fg_index_build_stats(const fg_index* ix, uint64_t* stats4);
+/* The same counters followed by {candidates bounded by the pass-1 sparse
+ * sketches, candidates those bounds rejected before their postings were
+ * read}; the first `count` of the 6 (zeros past them). */
+int fg_index_build_stats_ex(const fg_index* ix, uint64_t* stats, uint32_t count);
 int fg_index_free(fg_index* ix);
 
 /* InsertParams (update.hpp:22-28). */

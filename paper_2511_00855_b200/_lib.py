@@ -65,6 +65,7 @@ def _declare(lib):
                                       A.u32p]),
         "fg_index_build_times": (C.c_int, [C.c_void_p, A.f64p]),
         "fg_index_build_stats": (C.c_int, [C.c_void_p, A.u64p]),
+        "fg_index_build_stats_ex": (C.c_int, [C.c_void_p, A.u64p, C.c_uint32]),
         "fg_index_serialize": (C.c_int, [C.c_void_p, C.c_char_p, A.u64p]),
         "fg_index_insert": (C.c_int, [C.c_void_p, P(A.CorpusView), P(A.InsertParams)]),
         "fg_index_deserialize": (C.c_int, [C.c_char_p, C.c_int, P(C.c_void_p), P(C.c_void_p)]),

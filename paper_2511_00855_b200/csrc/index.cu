@@ -678,6 +678,14 @@ int fg_index_build_stats(const fg_index* ix, uint64_t* stats4) {
     });
 }
 
+int fg_index_build_stats_ex(const fg_index* ix, uint64_t* stats, uint32_t count) {
+    return guarded([&] {
+        if (!ix || !stats) throw Error("invalid-argument", "null pointer");
+        for (uint32_t i = 0; i < count && i < 6; ++i) stats[i] = ix->knn_stats[i];
+        for (uint32_t i = 6; i < count; ++i) stats[i] = 0;
+    });
+}
+
 int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p, fg_index** out) {
     return guarded([&] {
         if (!c || !p || !out) throw Error("invalid-argument", "null pointer");
@@ -707,6 +715,8 @@ int fg_index_build(fg_corpus* c, const fg_kg_view* kg, const fg_build_params* p,
         ix->knn_stats[1] = ks.candidates;
         ix->knn_stats[2] = ks.dense_rows;
         ix->knn_stats[3] = static_cast<uint64_t>(ks.pass_seconds * 1e6);
+        ix->knn_stats[4] = ks.sketched;
+        ix->knn_stats[5] = ks.sketch_rejected;
         FGB_CUDA(cudaStreamSynchronize(s));
         ix->build_seconds[0] = secs(t0);
 

@@ -40,7 +40,9 @@ struct fg_index {
     std::vector<uint32_t> triplets;  // KnowledgeGraph::triplets(): (s, r, t) sorted, unique
     uint32_t max_kw_edges = 0, max_logical_group = 0;
     double build_seconds[5] = {0, 0, 0, 0, 0};
-    uint64_t knn_stats[4] = {0, 0, 0, 0};  // passes, candidates scored, dense rows, pass-kernel microseconds
+    // passes, candidates scored, dense rows, pass-kernel microseconds,
+    // candidates bounded by sparse sketches, candidates the sketches rejected
+    uint64_t knn_stats[6] = {0, 0, 0, 0, 0, 0};
 
     // search scratch + batch buffers: shared by every index on the device
     // (fgb::search_workspace), grown on demand, reused across calls

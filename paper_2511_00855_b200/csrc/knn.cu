@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
         if (a.timing && v) atomicAdd(&a.timing[slot], static_cast<unsigned long long>(v));
     };
     uint32_t cand_total = 0, dense_rows = 0;  // (thread 0 / lane 0 of each warp)
+    uint32_t sk_total = 0, sk_rej = 0;        // candidates sketched (thread 0) / rejected by it (lane 0)
 
     for (uint32_t j = tid; j < k; j += nt) {
         T_id[j] = a.L_ids[u * k + j];
@@ -894,6 +895,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     __syncthreads();
     const uint32_t n_c = n_cand;
     cand_total += n_c;
+    if (a.sketch) sk_total += n_c;
     // Sketch ORDER (NQ4 > 0 with sketches, when the pool has room): every
     // candidate's sketch bound is computed first and stored (bf16 rounded
     // up, above the compacted list); the ~kSkFirst candidates with the
@@ -929,9 +931,12 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
             // stored sketch bounds (+ |u||v| + 2 eps, rounded up) screen first
             const bool live = cand && !(bnd && static_cast<double>(__bfloat162float(
                                                    __ushort_as_bfloat16(bnd[s]))) < tau_lo);
-            if (a.timing && bnd) {
+            if ((a.timing || a.counts) && bnd) {
                 const uint32_t rej = __popc(__ballot_sync(approx::kFull, cand && !live));
-                if (lane == 0) count(kKnSketch, rej);
+                if (lane == 0) {
+                    count(kKnSketch, rej);
+                    sk_rej += rej;
+                }
             }
             const uint32_t fm = __ballot_sync(approx::kFull, live);
             uint32_t F = __popc(fm);
@@ -948,7 +953,10 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
                                                               static_cast<double>(sb) * sk_scale, 0.0) +
                                                 2.0 * eps < tau_lo);
                 const uint32_t pm = __ballot_sync(approx::kFull, pass);
-                if (lane == 0) count(kKnSketch, F - __popc(pm));
+                if (lane == 0) {
+                    count(kKnSketch, F - __popc(pm));
+                    sk_rej += F - __popc(pm);
+                }
                 const uint32_t s2 = __fns(pm, 0, lane + 1);
                 const uint32_t sl = s2 < 32 ? s2 : 0;
                 cn = __shfl_sync(approx::kFull, cn, sl);
@@ -1177,6 +1185,8 @@ __global__ void __launch_bounds__(kPassThreads, 2) knn_pass_kernel(PassArgs a) {
     if (a.counts) {
         if (tid == 0) atomicAdd(&a.counts[0], static_cast<unsigned long long>(cand_total));
         if (lane == 0 && dense_rows) atomicAdd(&a.counts[1], static_cast<unsigned long long>(dense_rows));
+        if (tid == 0 && sk_total) atomicAdd(&a.counts[2], static_cast<unsigned long long>(sk_total));
+        if (lane == 0 && sk_rej) atomicAdd(&a.counts[3], static_cast<unsigned long long>(sk_rej));
     }
 }
 
@@ -1384,7 +1394,7 @@ void knn_pass_range(const fg_corpus& c, const DevKnn& g, const ReverseLists& R, 
                R.ids.get(),    R.fresh.get(), R.cnt.get(),  next.ids.get(), next.scores.get(),
                next.fresh.get(), d_changed, 0, lcap, scap, lo,
                0.0, 0.0, 0.0, 0.0, 0, nullptr, 0, kSortMin, 1, 32, nullptr, nullptr, nullptr};
-    if (R.counts.size() == 2) a.counts = R.counts.get();
+    if (R.counts.size() == 4) a.counts = R.counts.get();
     // (results do not depend on the order nodes are processed in)
     if (R.order.size() == g.n && lo == 0 && hi == g.n) a.order = R.order.get();
     if (const char* e = std::getenv("FGB_KNN_SORT_MIN")) a.sort_min = std::max(1, std::atoi(e));
@@ -1591,7 +1601,7 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
     uint32_t passes = 0;
     ReverseLists R;
     if (stats) {
-        R.counts.alloc(2);
+        R.counts.alloc(4);
         R.counts.zero(s);
     }
     DevKnn next;
@@ -1619,12 +1629,14 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
         }
     }
     if (stats) {
-        unsigned long long h[2] = {0, 0};
-        R.counts.download(h, 2, s);
+        unsigned long long h[4] = {0, 0, 0, 0};
+        R.counts.download(h, 4, s);
         FGB_CUDA(cudaStreamSynchronize(s));
         stats->passes = passes;
         stats->candidates = h[0];
         stats->dense_rows = h[1];
+        stats->sketched = h[2];
+        stats->sketch_rejected = h[3];
         stats->pass_seconds = R.pass_ms / 1e3;
     }
     return passes;

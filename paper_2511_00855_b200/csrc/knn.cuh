@@ -63,6 +63,7 @@ struct ReverseLists {
 // screening, device seconds of the pass kernels.
 struct KnnStats {
     uint64_t passes = 0, candidates = 0, dense_rows = 0;
+    uint64_t sketched = 0, sketch_rejected = 0;  // candidates bounded by sketches / rejected by them
     double pass_seconds = 0.0;
 };
 

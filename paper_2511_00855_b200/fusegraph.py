@@ -228,9 +228,10 @@ class HybridIndex:
         return dict(knn=t[0], refine=t[1], logical=t[2], norm_order=t[3], total=t[4])
 
     def build_stats(self) -> dict:
-        t = np.zeros(4, np.uint64)
-        check(lib().fg_index_build_stats(self.h, A.ptr(t, A.u64p)))
-        return dict(passes=int(t[0]), candidates=int(t[1]), dense_rows=int(t[2]), pass_seconds=int(t[3]) / 1e6)
+        t = np.zeros(6, np.uint64)
+        check(lib().fg_index_build_stats_ex(self.h, A.ptr(t, A.u64p), 6))
+        return dict(passes=int(t[0]), candidates=int(t[1]), dense_rows=int(t[2]), pass_seconds=int(t[3]) / 1e6,
+                    sketched=int(t[4]), sketch_rejected=int(t[5]))
 
     def last_search_stats(self):
         ms, launches = C.c_double(), C.c_uint64()
