@@ -163,7 +163,7 @@ void build_sharded(fg_index& ix, const fg_build_params& p, const Shards& sh, cud
     const int sk_policy = knn_sketch_policy();
     if (sk_policy >= 1) knn_sketch_prepare(c, R, s);  // (sketches of the whole replicated corpus)
     for (uint32_t it = 0; it < p.knn_iterations; ++it) {
-        if (it == 1 && sk_policy == 1) knn_sketch_disable(R);
+        if (it == knn_sketch_passes() && sk_policy == 1) knn_sketch_disable(R);
         knn_reverse_lists(g, R, s);
         if (it == 0) alloc_padded(next, n, sh.n_pad, k);
         changed.zero(s);

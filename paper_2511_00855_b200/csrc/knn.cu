@@ -1357,6 +1357,11 @@ int knn_sketch_policy() {
     return e ? std::atoi(e) : 1;
 }
 
+uint32_t knn_sketch_passes() {
+    const char* e = std::getenv("FGB_KNN_SKETCH_PASSES");  // dev A/B: passes screened under policy 1
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u;
+}
+
 void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s) {
     R.sk_paths = (c.max_lnnz ? 1u : 0u) | (c.max_snnz ? 2u : 0u);
     if (!R.sk_paths || !c.dc.meta || pass_nq4(c.dstride) == 0) return;  // (exact-chain passes: no screening)
@@ -1617,7 +1622,7 @@ uint32_t knn_build_device(const fg_corpus& c, uint32_t k_req, uint32_t max_itera
         ++passes;
         // pass 1's candidates are random: the sketch bound rejects most of
         // them; later passes score neighbourhoods, where it rarely does
-        if (it == 0 && sk_policy == 1) knn_sketch_disable(R);
+        if (it + 1 == knn_sketch_passes() && sk_policy == 1) knn_sketch_disable(R);
         if (static_cast<double>(changed) / denom < convergence) break;
         // After pass 1 the lists are neighbourhoods: later passes visit the
         // nodes in BFS order over them, so the CTAs resident at one time work

@@ -74,6 +74,7 @@ void knn_reverse_lists(const DevKnn& g, ReverseLists& R, cudaStream_t s);
 // (default), 2 = every pass incl. single fg_knn_iterate calls) and the
 // sketches themselves (built into R).
 int knn_sketch_policy();
+uint32_t knn_sketch_passes();  // passes screened under policy 1 (1)
 void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s);
 // Stops the screening for the next passes; the sketches stay allocated until R
 // dies (a device free synchronises the whole device, which would stall the
