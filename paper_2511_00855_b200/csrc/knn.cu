@@ -246,7 +246,9 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
     const uint32_t rs = a.c.dstride + 1, n4 = a.c.dstride >> 2;
     // rows + each entry's two sparse-chain results (the dense and the sparse
     // chains of an entry run on different threads)
-    const uint32_t cap = area_bytes < 16 ? 0u : static_cast<uint32_t>((area_bytes - 16) / (rs * 4ull + 16));
+    const uint32_t sub = nt / 3;  // entries per sub-batch (three chains each)
+    const size_t xbytes = static_cast<size_t>(sub) * 16 + 16;
+    const uint32_t cap = area_bytes < xbytes ? 0u : static_cast<uint32_t>((area_bytes - xbytes) / (rs * 4ull));
     float* rows = reinterpret_cast<float*>(area);
     double* xsp = reinterpret_cast<double*>(area + ((static_cast<size_t>(cap) * rs * 4 + 15) & ~size_t(15)));
     auto node_of = [&](uint32_t code) { return (code >> 31) ? T_id[code & 0x7FFFFFFFu] : S_id[code]; };
@@ -265,9 +267,16 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
         __syncthreads();
         return;
     }
-    for (uint32_t b0 = 0; b0 < n; b0 += cap) {
-        const uint32_t nb = min(cap, n - b0);
-        for (uint32_t r = warp; r < nb; r += nwarps) {
+    // a chunk covers max(cap, sub) entries: the dense rows of the first cap
+    // are staged in shared memory, the others' chains stream their rows from
+    // L2 (prefetched in bulk first), so all of a chunk's chains run at once
+    const uint32_t span = max(cap, sub);
+    for (uint32_t b0 = 0; b0 < n; b0 += span) {
+        const uint32_t nb = min(span, n - b0);
+        const uint32_t staged = min(nb, cap);
+        for (uint32_t r = staged + tid; r < nb; r += nt)
+            l2_prefetch(a.c.dense + static_cast<uint64_t>(node_of(fix[b0 + r])) * a.c.dstride, a.c.dstride * 4);
+        for (uint32_t r = warp; r < staged; r += nwarps) {
             const float4* src =
                 reinterpret_cast<const float4*>(a.c.dense + static_cast<uint64_t>(node_of(fix[b0 + r])) * a.c.dstride);
             float4 v[NQ4];
@@ -290,7 +299,6 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
         // adds their results in order): per sub-batch of up to nt/3 entries,
         // thread r runs entry r's dense chain while threads nbs + r and
         // 2 nbs + r run its learned and statistical chains
-        const uint32_t sub = nt / 3;
         for (uint32_t s0 = 0; s0 < nb; s0 += sub) {
             const uint32_t nbs = min(sub, nb - s0);
             if (tid >= nbs && tid < 3 * nbs) {
@@ -306,11 +314,28 @@ __device__ void exact_entries(const PassArgs& a, const SmemQuery& sq, const uint
                 xsp[2 * (r - s0) + (lp ? 0 : 1)] = x;
             }
             double acc = 0.0;
-            if (tid < nbs) {
+            if (tid < nbs && s0 + tid < staged) {
                 const float* row = rows + (s0 + tid) * rs;
 #pragma unroll 8
                 for (uint32_t j = 0; j < a.c.dstride; ++j)
                     acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(row[j])));
+            } else if (tid < nbs) {  // streamed row, 8 x 16 B in flight
+                const float4* src = reinterpret_cast<const float4*>(
+                    a.c.dense + static_cast<uint64_t>(node_of(fix[b0 + s0 + tid])) * a.c.dstride);
+                for (uint32_t j4 = 0; j4 < n4; j4 += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) v[q] = __ldg(src + min(j4 + q, n4 - 1));
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (j4 + q < n4) {
+                            const uint32_t j = 4 * (j4 + q);
+                            acc = __dadd_rn(acc, __dmul_rn(sq.dense[j], static_cast<double>(v[q].x)));
+                            acc = __dadd_rn(acc, __dmul_rn(sq.dense[j + 1], static_cast<double>(v[q].y)));
+                            acc = __dadd_rn(acc, __dmul_rn(sq.dense[j + 2], static_cast<double>(v[q].z)));
+                            acc = __dadd_rn(acc, __dmul_rn(sq.dense[j + 3], static_cast<double>(v[q].w)));
+                        }
+                }
             }
             __syncthreads();
             if (tid < nbs) {
