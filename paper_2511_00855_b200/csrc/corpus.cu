@@ -589,7 +589,8 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             }
         } else {
             PinnedStage st;
-            if (c->dim == c->dstride) {
+            const char* le = std::getenv("FGB_UPLOAD_LOCK");  // dev A/B: 0 = dense rows through the pinned stage
+            if (c->dim == c->dstride && !(le && le[0] == '0')) {
                 upload_locked(c->dense, v->dense, n * c->dstride, s);
             } else {
                 c->dense.ensure(n * c->dstride);
