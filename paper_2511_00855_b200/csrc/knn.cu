@@ -156,14 +156,24 @@ __device__ __forceinline__ double sketch_gv(unsigned int gmax_bits) {
     return static_cast<double>(__uint_as_float(gmax_bits)) * 1.001 / 3.0;
 }
 
-// Corpus max |value| of one sparse path (non-negative floats order like their bits).
-__global__ void sketch_max_kernel(const float* v, uint64_t m, unsigned int* out) {
+// Max |value| over the rows of c (both sparse paths; through the per-row
+// offsets, so a row view of a larger corpus — the insert path's batch — sees
+// exactly its own postings).  Non-negative floats order like their bits.
+__global__ void sketch_max_kernel(DevCorpus c, uint32_t paths, unsigned int* out) {
     float mx = 0.f;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
-        mx = fmaxf(mx, fabsf(v[i]));
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t doc = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); doc < c.n; doc += warps)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            if (!((paths >> p) & 1u)) continue;
+            const uint64_t off = p ? c.s_off[doc] : c.l_off[doc];
+            const uint32_t nnz = p ? c.s_nnz[doc] : c.l_nnz[doc];
+            for (uint32_t j = lane; j < nnz; j += 32) mx = fmaxf(mx, fabsf((p ? c.s_val : c.l_val)[off + j]));
+        }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-    if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
+    if (lane == 0 && mx > 0.f) atomicMax(out, __float_as_uint(mx));
 }
 
 // One warp per document: bucket maxima of |value| quantised up to 2 bits,
@@ -1399,10 +1409,7 @@ void knn_sketch_prepare(const fg_corpus& c, ReverseLists& R, cudaStream_t s) {
     R.sketch.alloc(c.n * (approx::kSketchBytes / 16));
     R.sk_gmax.alloc(1);
     R.sk_gmax.zero(s);
-    if (c.max_lnnz)
-        sketch_max_kernel<<<1184, 256, 0, s>>>(c.dc.l_val, c.l_nnz_total4 * 4, R.sk_gmax.get());
-    if (c.max_snnz)
-        sketch_max_kernel<<<1184, 256, 0, s>>>(c.dc.s_val, c.s_nnz_total4 * 4, R.sk_gmax.get());
+    sketch_max_kernel<<<1184, 256, 0, s>>>(c.dc, R.sk_paths, R.sk_gmax.get());
     FGB_LAUNCH("sketch_max_kernel");
     constexpr uint32_t kWarps = 4;  // 32 KB of bucket maxima per CTA
     sketch_build_kernel<<<(unsigned)((c.n + kWarps - 1) / kWarps), 32 * kWarps, kWarps * approx::kSketchBuckets * 4, s>>>(

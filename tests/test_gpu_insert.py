@@ -97,3 +97,22 @@ def test_insert_cost_at_scale():
           f"recall rebuild {rec(rf):.4f} insert {rec(ri):.4f}")
     assert rec(ri) >= rec(rf) - 0.02
     assert insert_s < 0.40 * rebuild_s
+
+
+def test_insert_batch_sketch_screening_identical(monkeypatch):
+    """A batch of >= 8,192 docs runs its batch-local NN-Descent (update.cpp:71-88)
+    with pass-1 sparse-sketch screening on a zero-copy row view of the grown
+    corpus (the sketch scale is taken over the view's own postings): the
+    resulting index equals the one built with the screening off."""
+    p = A.synth_params(docs=13000, dense_dim=64, clusters=20, cluster_spread=0.25, learned_vocab=5000,
+                       learned_nnz=24, statistical_vocab=8000, statistical_nnz=12, seed=71)
+    c, kg, _ = synth.generate_corpus(p, 0)
+    base, extra = part(c, np.arange(4000)), part(c, np.arange(4000, c.n))
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("FGB_KNN_SKETCH", mode)
+        ix = fg.build_hybrid_index(fg.DeviceCorpus(base), kg, degree=16, knn_k=32, seed=7100)
+        ix.insert(extra)
+        out[mode] = ix.export()
+        ix.close()
+    same(out["1"], out["0"])
