@@ -589,8 +589,13 @@ int fg_corpus_upload(const fg_corpus_view* v, int device, fg_corpus** out) {
             }
         } else {
             PinnedStage st;
-            const char* le = std::getenv("FGB_UPLOAD_LOCK");  // dev A/B: 0 = dense rows through the pinned stage
-            if (c->dim == c->dstride && !(le && le[0] == '0')) {
+            // unpadded rows up to 4 GB: page-locked in place (1M docs: 0.38-0.40 s
+            // vs 0.45 s through the stage); larger corpora through the pinned
+            // stage (10M docs: 4.2-4.7 s vs 6.5 s — locking 30 GB of pages costs
+            // more than the staged copies; tools/upload_probe.py)
+            const char* le = std::getenv("FGB_UPLOAD_LOCK");  // dev A/B: 0 = stage, 1 = lock
+            const bool lock = le ? le[0] != '0' : n * c->dstride * 4ull <= (4ull << 30);
+            if (c->dim == c->dstride && lock) {
                 upload_locked(c->dense, v->dense, n * c->dstride, s);
             } else {
                 c->dense.ensure(n * c->dstride);
